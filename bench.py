@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""KITC hot-path benchmark (driver contract).
+
+Step = one pass of the whole hot path over one synthetic input: tree build +
+modified weights (this rank's cluster shard) [+ NCCL all-gather of fhat] +
+treecode evaluation of this rank's targets, for BASELINE.json config C3
+(N = 1e6 uniform, Stokeslet, n = 8, theta = 0.7, N0 = 2000, eps = 0.01).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
+  python bench.py --impl reference ...   # the CPU oracle, bounded sample
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import kitc_inputs as KI  # noqa: E402
+
+METRIC = "KITC Stokeslet targets/s, N=1e6 n=8 θ=0.7, 1/2/4/8 B200; % of FP64 peak"
+UNIT = "targets/s"
+FLOPS_PER_PAIR = {0: 32, 1: 59, 2: 91}   # algorithmic flops per pair
+PEAK_SMS, PEAK_FMA_PER_CLK = 148, 64     # B200: 148 SMs x 64 FP64 FMA/clk/SM
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kitc", choices=["kitc", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip E vs the GPU direct sum")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (recipe's clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.path = os.path.join("/tmp", f"kitc_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle leg
+def oracle_sample(cfg, X, W, S_targets, weight_frac=0.1, seed=1, fhat=None):
+    """Bounded sample of the CPU oracle on the workload: full tree build,
+    Algorithm 1 on a set of clusters holding >= weight_frac of sum N_C
+    (extrapolated by sum N_C), Algorithm 2 on S_targets random targets
+    (extrapolated by N / S).  Returns (targets/s, detail)."""
+    import oracle as O
+    N = cfg["N"]
+    t0 = time.perf_counter()
+    T = O.Tree(X, cfg["N0"])
+    t_tree = time.perf_counter() - t0
+    sizes = T.end - T.begin
+    tot = float(sizes[1:].sum())        # root skipped on both sides (reading A16)
+    cb = T.nclusters
+    acc = 0.0
+    while cb > 1 and acc < weight_frac * tot:
+        cb -= 1
+        acc += sizes[cb]
+    F = np.zeros((T.nclusters, 3, (cfg["n"] + 1) ** 3)) if fhat is None else fhat.copy()
+    t0 = time.perf_counter()
+    T.modified_weights(W, cfg["n"], cluster_range=(cb, T.nclusters), out=F)
+    t_w = (time.perf_counter() - t0) * tot / acc
+    if fhat is None:
+        F = T.modified_weights(W, cfg["n"], cluster_range=(1, T.nclusters), out=F)
+    tg = KI.sample_targets(N, S_targets, seed=seed)
+    t0 = time.perf_counter()
+    T.treecode(cfg["kernel"], cfg["eps"], cfg["n"], cfg["theta"], W, fhat=F, targets=tg)
+    t_e = (time.perf_counter() - t0) * N / len(tg)
+    total = t_tree + t_w + t_e
+    return N / total, dict(t_tree_s=t_tree, t_weights_s_extrapolated=t_w, t_eval_s_extrapolated=t_e,
+                           weight_clusters=int(T.nclusters - cb), eval_targets=int(len(tg))), F
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    X, W = KI.config_particles(args.config)
+    import oracle as O
+    O.build()
+    # untimed setup: full modified weights so the sampled evaluation reads real data
+    _, _, F = oracle_sample(cfg, X, W, 50, weight_frac=0.0)
+    S = 400
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        v, det, _ = oracle_sample(cfg, X, W, S, seed=100 + i, fhat=F)
+        if i >= args.warmup:
+            times.append(cfg["N"] / v)
+    tstep = sum(times) / len(times)
+    val = cfg["N"] / tstep
+    sample = (f"per step: full oracle tree build; Algorithm 1 on the last clusters holding >=10% of "
+              f"sum N_C (time x sum N_C ratio); Algorithm 2 on {S} random targets (time x N/{S})")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tstep * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (kitc_inputs, seed 0)",
+            "config": {"workload": f"{args.config}: " + json.dumps(cfg), "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_kitc(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1902_02250_b200 import dist as D
+    from paper_1902_02250_b200 import kitc
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    kern, n, theta, N0, eps, N = cfg["kernel"], cfg["n"], cfg["theta"], cfg["N0"], cfg["eps"], cfg["N"]
+    m, p = kitc.kitc_kernel_dims(kern)
+    P3 = (n + 1) ** 3
+    X, W = KI.config_particles(args.config)
+    Xd = torch.from_numpy(X).to(dev)
+    Wd = torch.from_numpy(W).to(dev)
+    T = kitc.Tree(Xd, N0)
+    C = T.nclusters
+    rg = T.export_ranges()
+    cshards = D.cluster_shards(rg["begin"], rg["end"], world, skip_root=True)
+    S = D.padded_shard_size(cshards)
+    prefix = [T.batch_targets(b) for b in range(T.nbatches + 1)] if world > 1 else [0, N]
+    bshards = D.batch_shards(prefix, world) if world > 1 else [(0, T.nbatches)]
+    cb, ce = cshards[rank]
+    bb, be = bshards[rank]
+    gathered = torch.zeros((world, S, m, P3), dtype=torch.float64, device=dev)
+    fhat = torch.zeros((C, m, P3), dtype=torch.float64, device=dev)
+    out = torch.zeros((N, p), dtype=torch.float64, device=dev)
+    row = m * P3 * 8
+    shard_base = gathered[rank].data_ptr() - cb * row    # virtual base: cluster c -> shard row c - cb
+    import ctypes as Cc
+
+    def weights():
+        if world == 1:
+            T.modified_weights(kern, n, Wd, cluster_range=(cb, ce), fhat=fhat)
+        else:
+            kitc.kitc_modified_weights(T.handle, kern, n, kitc._ptr(Wd), cb, ce, Cc.c_void_p(shard_base),
+                                       kitc._stream())
+            D.all_gather_fhat(fhat, gathered, gathered[rank], cshards, rank)
+
+    ev_e0, ev_e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step(Xsrc=None, timed_eval=False):
+        T.build(Xd if Xsrc is None else Xsrc, N0)
+        weights()
+        if timed_eval:
+            ev_e0.record(stream)
+        T.eval(kern, n, theta, eps, fhat, out=out, batch_range=(bb, be))
+        if timed_eval:
+            ev_e1.record(stream)
+
+    # algorithmic work of this rank's eval launch (interaction counts, deterministic)
+    step()
+    _, st = T.eval(kern, n, theta, eps, fhat, batch_range=(bb, be), stats=True)
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    pairs = int(st[:, 1].sum() + st[:, 3].sum())
+    flops_eval = pairs * FLOPS_PER_PAIR[kern]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    l0 = kitc.kitc_launch_count()
+    tot_ms, eval_ms = 0.0, 0.0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(args.steps):
+        flush.zero_()                               # L2 flushed between timed steps (untimed)
+        e0.record(stream)
+        step(timed_eval=True)
+        e1.record(stream)
+        e1.synchronize()
+        tot_ms += e0.elapsed_time(e1)
+        eval_ms += ev_e0.elapsed_time(ev_e1)
+    launches = kitc.kitc_launch_count() - l0
+    barrier()
+    clocks = clk.stop()
+    t = torch.tensor([tot_ms, eval_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t[0]) / args.steps
+    value = N / (ms_step / 1e3)
+    eval_launch_ms = eval_ms / args.steps
+
+    # e2e: host buffers through the C ABI, H2D + step + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(X).pin_memory()
+        Wh = torch.from_numpy(W).pin_memory()
+        outh = torch.empty((N, p), dtype=torch.float64).pin_memory()
+        Xe = torch.empty_like(Xd)
+
+        def e2e_step():
+            Xe.copy_(Xh, non_blocking=True)
+            Wd.copy_(Wh, non_blocking=True)
+            step(Xsrc=Xe)
+            outh.copy_(out, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        tot = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        tt = torch.tensor([tot], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt[0]) / args.steps
+        e2e = {"value": N / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(X.nbytes + W.nbytes), "d2h_bytes_per_step": int(N * p * 8)}
+
+    # accuracy of this run vs the GPU direct sum (outside every timed region)
+    check = None
+    if not args.no_check and world == 1:
+        ref = kitc.direct(Xd, Wd, kern, eps)
+        check = {"E_vs_gpu_direct": kitc.rel_error(ref, out)}
+
+    if rank != 0:
+        return
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    smax = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_tflops = PEAK_SMS * PEAK_FMA_PER_CLK * 2 * smax * 1e6 / 1e12
+    achieved = flops_eval / (eval_launch_ms * 1e-3) / 1e12
+    roof = {"bound": "alu", "kernel": "k_eval (treecode evaluation)", "achieved": achieved,
+            "peak": peak_tflops, "unit": "TFLOP/s", "frac": achieved / peak_tflops, "traffic": None,
+            "peak_source": f"derived: {PEAK_SMS} SMs x {PEAK_FMA_PER_CLK} FP64 FMA/clk x 2 x {smax:.0f} MHz "
+                           "(DFMA probe measured 34.1 TFLOP/s, profiles/r01_fp64_peak.txt)",
+            "algorithmic_flops_per_launch": flops_eval, "pairs_per_launch": pairs,
+            "flops_per_pair": FLOPS_PER_PAIR[kern], "launch_ms": eval_launch_ms,
+            "step_share": eval_launch_ms / ms_step}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        O.build()
+        v, det, _ = oracle_sample(cfg, X, W, 1500)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": "full oracle tree; Algorithm 1 on clusters holding >=10% of sum N_C "
+                         "(x sum N_C ratio); Algorithm 2 on 1500 random targets (x N/1500)", **det}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (kitc_inputs: uniform [-1,1]^3, seed 0)",
+            "config": {"workload": f"{args.config} ({KI.CONFIGS[args.config]})",
+                       "parallelism": f"tree replicated, fhat sharded + NCCL all-gather, targets dp{world}",
+                       "l2": "flushed between timed steps (256 MB write, untimed)",
+                       "clusters": C, "depth": T.depth, "batches": T.nbatches},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks, "check": check}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = dict(KI.CONFIGS[args.config])
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_kitc(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * kitc.h -- C ABI of libkitc.so, the B200 (sm_100a) hot path of the
+ * barycentric Lagrange kernel-independent treecode (KITC) of Wang, Krasny and
+ * Tlupova, arXiv:1902.02250.  P:<n> = PAPER.md line n.
+ *
+ * The library computes, for targets = sources x_i (i = 0..N-1),
+ *     u(x_i) = sum_j k(x_i, x_j) f_j                       (Eq. N-body)
+ * with the particle-cluster treecode of Algorithm 2: a tree of
+ * rectangular clusters, modified weights at (n+1)^3 Chebyshev
+ * points per cluster (Eq. modified_weights, Algorithm 1),
+ * and a per-target traversal under the MAC r/R <= theta (Eq. MAC)
+ * summing far clusters through their proxies (Eq. pc_approximation_3D,
+ * P:436-440) and near leaves directly (Eq. pc_interaction_3D).
+ * Kernels: the regularized Stokeslet (Eq. Velocity_1), the rotlet
+ * (Eqs. Velocity_2 / AngularVelocity with f = 0) and the combined
+ * Stokeslet+rotlet.  kitc_direct is the O(N^2) sum.
+ *
+ * Conventions (all entry points):
+ *  - Pointers named *_dev are CUDA device pointers; *_host are host pointers.
+ *    The CALLER owns every buffer passed in.  A kitc_tree handle owns the
+ *    device memory of the tree it holds (allocated stream-ordered from the
+ *    device's default memory pool on the stream of kitc_build_tree, retained
+ *    and reused across rebuilds, released by kitc_tree_free).
+ *  - Layouts: coordinates are AoS double[N][3]; weights are AoS double[N][m];
+ *    outputs are AoS double[N][p]; all in the caller's ORIGINAL particle order.
+ *  - Work is enqueued on the caller's stream `s` (cudaStream_t passed as void*;
+ *    NULL = legacy default stream).  Only kitc_build_tree and kitc_tree_export
+ *    synchronize that stream.
+ *  - Errors never cross the ABI as exceptions: every call returns a
+ *    kitc_status; kitc_last_error() returns a thread-local message for the
+ *    last non-OK status.  KITC_ECUDA is returned for launch or asynchronous
+ *    CUDA errors observed by the call.
+ *  - Everything is fp64.  Results are deterministic: bitwise identical run to
+ *    run and independent of how batch / cluster ranges are split across calls
+ *    or ranks.
+ */
+#ifndef KITC_H
+#define KITC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KITC_OK = 0,
+    KITC_EINVAL = -1, /* bad argument (range, NULL, non-finite coordinate, ...) */
+    KITC_ENOMEM = -2, /* device or host allocation failed */
+    KITC_ECUDA = -3,  /* CUDA launch / runtime error */
+    KITC_ESTATE = -4  /* call order violated (e.g. eval before weights) */
+} kitc_status;
+
+typedef enum {
+    KITC_STOKESLET = 0,         /* m = 3 (force f),  p = 3 (u)         Eq. Velocity_1 */
+    KITC_ROTLET = 1,            /* m = 3 (torque n), p = 6 (u, w)      Eqs. Velocity_2/AngularVelocity, f = 0 */
+    KITC_STOKESLET_ROTLET = 2   /* m = 6 (f, n),     p = 6 (u, w)      Eqs. Velocity_2/AngularVelocity */
+} kitc_kernel;
+
+typedef enum {
+    KITC_SELF_OMIT = 0,   /* skip j == i (by index) -- BASELINE configs, reading A8 */
+    KITC_SELF_INCLUDE = 1 /* sum over all j (the regularized kernels are finite at r = 0) */
+} kitc_self;
+
+typedef struct kitc_tree kitc_tree; /* opaque, library-owned handle */
+
+/* Weight and output dimensions (m, p) of a kernel.  EINVAL for unknown k. */
+kitc_status kitc_kernel_dims(int32_t kernel, int32_t* m, int32_t* p);
+
+/* Create an empty tree handle (no device memory yet).  *out = NULL on error. */
+kitc_status kitc_tree_create(kitc_tree** out);
+
+/* Build the cluster tree of N particles (Algorithm 2 line 5; rule
+ * P:583-596 with DESIGN.md readings A1-A4): every cluster's box is the minimal
+ * bounding box of its particles; a cluster with count > N0 is bisected at its
+ * midpoint along every side longer than lmax/sqrt(2) (lmax = its own longest
+ * side), particles with x_l >= mid go to the upper half; children are the
+ * nonempty groups in ascending code bx|by<<1|bz<<2, stably partitioned; a
+ * cluster whose split leaves one nonempty child (or lmax = 0) stays a leaf.
+ *  xyz_dev: device, double[N][3], original order, finite (else EINVAL).
+ *  N in [1, 2^31 - 1], N0 >= 1.  Rebuilding an existing handle is allowed.
+ * Synchronizes the stream (one small device->host read per tree level). */
+kitc_status kitc_build_tree(kitc_tree* t, const double* xyz_dev, int64_t N, int32_t N0, void* s);
+
+/* Sizes of the built tree.  Any output pointer may be NULL.
+ *  n_clusters: number of clusters C (BFS order: by level, then by range start);
+ *  depth: deepest level (root = 0); n_batches: number of 32-target batches
+ *  (batches never straddle a leaf; ordered by target position);
+ *  n_degenerate: leaves with count > N0 (coincident points). */
+kitc_status kitc_tree_info(const kitc_tree* t, int64_t* n_clusters, int32_t* depth,
+                           int64_t* n_batches, int32_t* n_degenerate);
+
+/* Copy the tree structure to host buffers (for parity checks; synchronizes).
+ * Any pointer may be NULL.  perm_host[N]: sorted position -> original index;
+ * per cluster (C entries): begin, end (sorted-index range), level, parent
+ * (-1 for the root), first_child (-1 for leaves; children are contiguous),
+ * nchild, lo_host[C][3], hi_host[C][3] (the minimal box). */
+kitc_status kitc_tree_export(const kitc_tree* t, int64_t* perm_host, int64_t* begin_host,
+                             int64_t* end_host, int32_t* level_host, int32_t* parent_host,
+                             int32_t* first_child_host, int32_t* nchild_host, double* lo_host,
+                             double* hi_host);
+
+/* Modified weights (Eq. modified_weights, Algorithm 1)
+ * of clusters [cluster_begin, cluster_end) at degree n in [1, 16]:
+ *   fhat_k = sum_{y_j in C} L_k1(y_j1) L_k2(y_j2) L_k3(y_j3) f_j
+ * with L in barycentric form (Eq. Barycentric-1D) on the cluster's Chebyshev
+ * grid s_{l,k} = c_l + h_l cos(k pi / n) (s_{l,0} = hi_l and s_{l,n} = lo_l
+ * exactly), simple weights (-1)^k delta_k, and the coincidence flag
+ * |y - s_k| <= DBL_MIN -> L = e_k (last k wins).
+ *  w_dev: device, double[N][m] in ORIGINAL order (m from kitc_kernel_dims).
+ *  fhat_dev: device, double[C][m][(n+1)^3] (k3 fastest); only the requested
+ *  clusters' slices are written.  Also gathers w into the tree's sorted
+ *  layout and computes every cluster's grid (both used by kitc_eval).
+ *  0 <= cluster_begin <= cluster_end <= C.  ESTATE if no tree is built. */
+kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const double* w_dev,
+                                  int64_t cluster_begin, int64_t cluster_end, double* fhat_dev,
+                                  void* s);
+
+/* Treecode evaluation (Algorithm 2 lines 7-17) for the targets of
+ * batches [batch_begin, batch_end): per target, depth-first over the tree;
+ * MAC accept iff R^2 > 0 and r^2 <= (theta*theta) R^2 (R = distance to the box
+ * centre, r = half-diagonal, all round-to-nearest, no FMA: DESIGN.md A4/A5);
+ * accepted -> far field over the (n+1)^3 proxies with fhat; rejected leaf ->
+ * direct sum over its particles (j == i skipped under KITC_SELF_OMIT);
+ * rejected internal -> children.
+ *  n, kernel: must match the last kitc_modified_weights call; N0 must equal
+ *  the tree's N0; 0 <= theta < 1; eps >= 0 (eps = 0 requires SELF_OMIT).
+ *  fhat_dev: the FULL double[C][m][(n+1)^3] (every cluster a target may accept).
+ *  out_dev: device double[N][p], original order; only the targets of the given
+ *  batches are written.
+ *  stats_dev: optional (NULL = off) device uint64[N][5], original order:
+ *  far clusters, far pairs, near leaves, near pairs, covered sources. */
+kitc_status kitc_eval(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0,
+                      double eps, int32_t self, const double* fhat_dev, int64_t batch_begin,
+                      int64_t batch_end, double* out_dev, uint64_t* stats_dev, void* s);
+
+/* Number of targets in batches [0, batch_end) -- for splitting work. */
+kitc_status kitc_batch_targets(const kitc_tree* t, int64_t batch_end, int64_t* n_targets);
+
+/* O(N^2) direct sum u(x_i) = sum_j k(x_i, y_j) f_j (Eq. N-body).
+ *  x_tgt_dev double[Nt][3], x_src_dev double[Ns][3], w_src_dev double[Ns][m],
+ *  out_dev double[Nt][p] (all device).  KITC_SELF_OMIT requires x_tgt_dev ==
+ *  x_src_dev and Nt == Ns (skip j == i); otherwise EINVAL. */
+kitc_status kitc_direct(int32_t kernel, double eps, int32_t self, const double* x_tgt_dev,
+                        int64_t Nt, const double* x_src_dev, const double* w_src_dev, int64_t Ns,
+                        double* out_dev, void* s);
+
+/* Relative error E (Eq. error) of approx vs ref, both device
+ * double[count] (rows of p components concatenated).  Writes E to
+ * *E_host (synchronizes).  EINVAL if the reference is identically zero. */
+kitc_status kitc_rel_error(const double* ref_dev, const double* approx_dev, int64_t count,
+                           double* E_host, void* s);
+
+/* Free the handle and its device memory (stream-ordered on the build stream). */
+void kitc_tree_free(kitc_tree* t);
+
+/* Thread-local message for the last non-OK status ("" if none). */
+const char* kitc_last_error(void);
+
+/* Number of CUDA kernels this library has launched in the process so far
+ * (monotone counter; bench.py reports the difference over the timed region). */
+uint64_t kitc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KITC_H */

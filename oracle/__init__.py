@@ -53,6 +53,7 @@ def lib():
         L.orc_tree_info.argtypes = [vp, C.POINTER(i64), C.POINTER(i32), C.POINTER(i32)]
         L.orc_tree_export.argtypes = [vp] + [vp] * 9
         L.orc_modified_weights.argtypes = [vp, i32, i32, vp, vp]
+        L.orc_modified_weights_range.argtypes = [vp, i32, i32, vp, i64, i64, vp]
         L.orc_modified_weights_box.argtypes = [i64, vp, vp, i32, i32, vp, vp, vp]
         L.orc_treecode.argtypes = [vp, i32, d, i32, d, i32, vp, vp, vp, i64, vp, vp]
         L.orc_direct.argtypes = [i32, d, i32, i32, i64, vp, vp, vp, i64, vp]
@@ -151,12 +152,16 @@ class Tree:
             _lib.orc_tree_free(h)
             self._h = None
 
-    def modified_weights(self, W, n):
+    def modified_weights(self, W, n, cluster_range=None, out=None):
         W = _f64(W)
         m = W.shape[1]
         P = n + 1
-        F = np.empty((self.nclusters, m, P * P * P))
-        assert lib().orc_modified_weights(self._h, n, m, _p(W), _p(F)) == 0
+        F = np.zeros((self.nclusters, m, P * P * P)) if out is None else out
+        if cluster_range is None:
+            assert lib().orc_modified_weights(self._h, n, m, _p(W), _p(F)) == 0
+        else:
+            cb, ce = cluster_range
+            assert lib().orc_modified_weights_range(self._h, n, m, _p(W), cb, ce, _p(F)) == 0
         return F
 
     def treecode(self, kernel, eps, n, theta, W, fhat=None, targets=None, self_omit=True,

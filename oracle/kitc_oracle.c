@@ -466,6 +466,21 @@ int orc_modified_weights(const orc_tree* T, int n, int m, const double* w, doubl
     return 0;
 }
 
+/* Same, for clusters [cb, ce) only (bounded-sample timing in bench.py). */
+int orc_modified_weights_range(const orc_tree* T, int n, int m, const double* w, int64_t cb,
+                               int64_t ce, double* fhat)
+{
+    if (n < 1 || n > 60 || m < 1 || cb < 0 || ce > T->nnodes || cb > ce) return -1;
+    int64_t N = T->N;
+    double* fs = (double*)malloc((size_t)N * m * sizeof(double));
+    for (int64_t s = 0; s < N; ++s)
+        for (int c = 0; c < m; ++c) fs[s * m + c] = w[T->perm[s] * m + c];
+    size_t per = (size_t)m * (n + 1) * (n + 1) * (n + 1);
+    for (int64_t i = cb; i < ce; ++i) alg1_cluster(&T->nodes[i], n, m, T->xs, fs, fhat + per * i);
+    free(fs);
+    return 0;
+}
+
 /* Modified weights of one explicit particle set on an explicit box (for the
  * moment-identity pins): y N x 3, f N x m, box lo/hi -> fhat m x (n+1)^3. */
 int orc_modified_weights_box(int64_t N, const double* y, const double* f, int m, int n,

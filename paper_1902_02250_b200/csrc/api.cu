@@ -1,0 +1,133 @@
+// api.cu -- the extern "C" entry points of libkitc.so (include/kitc.h).
+// Argument checks + exception barrier; the work is in tree.cu, weights.cu,
+// eval.cu and direct.cu.
+#include <new>
+
+#include "kitc_internal.cuh"
+
+using namespace kitc;
+
+#define KITC_GUARD(...)                                                        \
+    try {                                                                       \
+        __VA_ARGS__                                                                 \
+    } catch (const std::bad_alloc&) {                                           \
+        return set_error(KITC_ENOMEM, "host allocation failed");                \
+    } catch (...) {                                                             \
+        return set_error(KITC_ECUDA, "unexpected C++ exception");               \
+    }
+
+extern "C" {
+
+kitc_status kitc_kernel_dims(int32_t kernel, int32_t* m, int32_t* p) {
+    int mm, pp;
+    switch (kernel) {
+        case KITC_STOKESLET: mm = 3; pp = 3; break;
+        case KITC_ROTLET: mm = 3; pp = 6; break;
+        case KITC_STOKESLET_ROTLET: mm = 6; pp = 6; break;
+        default: return set_error(KITC_EINVAL, "unknown kernel");
+    }
+    if (m) *m = mm;
+    if (p) *p = pp;
+    return KITC_OK;
+}
+
+kitc_status kitc_tree_create(kitc_tree** out) {
+    if (!out) return set_error(KITC_EINVAL, "kitc_tree_create: out is NULL");
+    *out = nullptr;
+    KITC_GUARD(*out = new kitc_tree(); return KITC_OK;)
+}
+
+kitc_status kitc_build_tree(kitc_tree* t, const double* xyz, int64_t N, int32_t N0, void* s) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_build_tree: NULL handle");
+    KITC_GUARD(return build_tree(t, xyz, N, N0, (cudaStream_t)s);)
+}
+
+kitc_status kitc_tree_info(const kitc_tree* t, int64_t* nc, int32_t* depth, int64_t* nb, int32_t* ndeg) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_tree_info: NULL handle");
+    if (!t->built) return set_error(KITC_ESTATE, "kitc_tree_info: tree not built");
+    if (nc) *nc = t->nclusters;
+    if (depth) *depth = t->depth;
+    if (nb) *nb = t->nbatches;
+    if (ndeg) *ndeg = t->ndegenerate;
+    return KITC_OK;
+}
+
+kitc_status kitc_tree_export(const kitc_tree* t, int64_t* perm, int64_t* begin, int64_t* end, int32_t* level,
+                             int32_t* parent, int32_t* first_child, int32_t* nchild, double* lo, double* hi) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_tree_export: NULL handle");
+    if (!t->built) return set_error(KITC_ESTATE, "kitc_tree_export: tree not built");
+    KITC_GUARD({
+        cudaStream_t s = t->stream;
+        const int64_t C = t->nclusters, N = t->N;
+        if (perm) {
+            std::vector<int> p(N);
+            KITC_CUDA(cudaMemcpyAsync(p.data(), t->perm.p, N * sizeof(int), cudaMemcpyDeviceToHost, s));
+            KITC_CUDA(cudaStreamSynchronize(s));
+            for (int64_t i = 0; i < N; ++i) perm[i] = p[i];
+        }
+        if (lo || hi) {
+            std::vector<double> b(C * 6);
+            KITC_CUDA(cudaMemcpyAsync(b.data(), t->box.p, C * 6 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            KITC_CUDA(cudaStreamSynchronize(s));
+            for (int64_t c = 0; c < C; ++c)
+                for (int l = 0; l < 3; ++l) {
+                    if (lo) lo[c * 3 + l] = b[c * 6 + l];
+                    if (hi) hi[c * 3 + l] = b[c * 6 + 3 + l];
+                }
+        }
+        for (int64_t c = 0; c < C; ++c) {
+            if (begin) begin[c] = t->h_begin[c];
+            if (end) end[c] = t->h_end[c];
+            if (level) level[c] = t->h_level[c];
+            if (parent) parent[c] = t->h_parent[c];
+            if (first_child) first_child[c] = t->h_first[c];
+            if (nchild) nchild[c] = t->h_nchild[c];
+        }
+        return KITC_OK;
+    })
+}
+
+kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const double* w, int64_t cb,
+                                  int64_t ce, double* fhat, void* s) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_modified_weights: NULL handle");
+    KITC_GUARD(return modified_weights(t, kernel, n, w, cb, ce, fhat, (cudaStream_t)s);)
+}
+
+kitc_status kitc_eval(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0, double eps,
+                      int32_t self, const double* fhat, int64_t bb, int64_t be, double* out, uint64_t* stats,
+                      void* s) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_eval: NULL handle");
+    if (t->built && N0 != t->N0) return set_error(KITC_EINVAL, "kitc_eval: N0 differs from the tree's N0");
+    KITC_GUARD(return eval(t, kernel, n, theta, eps, self, fhat, bb, be, out, stats, (cudaStream_t)s);)
+}
+
+kitc_status kitc_batch_targets(const kitc_tree* t, int64_t be, int64_t* nt) {
+    if (!t || !nt) return set_error(KITC_EINVAL, "kitc_batch_targets: NULL argument");
+    if (!t->built) return set_error(KITC_ESTATE, "kitc_batch_targets: tree not built");
+    if (be < 0 || be > t->nbatches) return set_error(KITC_EINVAL, "kitc_batch_targets: bad batch index");
+    *nt = t->h_bprefix[be];
+    return KITC_OK;
+}
+
+kitc_status kitc_direct(int32_t kernel, double eps, int32_t self, const double* xt, int64_t Nt, const double* xs,
+                        const double* ws, int64_t Ns, double* out, void* s) {
+    KITC_GUARD(return direct(kernel, eps, self, xt, Nt, xs, ws, Ns, out, (cudaStream_t)s);)
+}
+
+kitc_status kitc_rel_error(const double* ref, const double* ap, int64_t n, double* E, void* s) {
+    KITC_GUARD(return rel_error(ref, ap, n, E, (cudaStream_t)s);)
+}
+
+void kitc_tree_free(kitc_tree* t) {
+    if (!t) return;
+    cudaStream_t s = t->stream;
+    for (DevBuf* b : {&t->x, &t->y, &t->z, &t->perm, &t->x2, &t->y2, &t->z2, &t->perm2, &t->w, &t->box, &t->cr,
+                      &t->topo, &t->grid, &t->bstart, &t->bcount, &t->d_items, &t->d_part, &t->d_cnt, &t->d_off,
+                      &t->d_lvl, &t->d_split, &t->d_flag, &t->d_witems, &t->d_wpart})
+        b->release(s);
+    t->h_stage.release();
+    t->h_cnt.release();
+    delete t;
+}
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+// direct.cu -- O(N^2) direct sum u(x_i) = sum_j k(x_i, y_j) f_j (Eq. N-body,
+// P:42-67) and the relative error E (Eq. error), sm_100a fp64.
+//
+// One thread per target; sources are staged through shared memory in tiles of
+// kTile (broadcast reads); each tile's contribution is summed into a tile
+// partial that is then added to the running total (two-level summation keeps
+// the rounding of N = 1e7 sums ~10x below the 1e-12 parity gate).
+#include <algorithm>
+#include <cmath>
+
+#include "kitc_internal.cuh"
+#include "pair.cuh"
+
+namespace kitc {
+
+namespace {
+
+constexpr int kTile = 256;
+
+template <int KER>
+__global__ void __launch_bounds__(kTile) k_direct(const double* __restrict__ xt, int Nt,
+                                                  const double* __restrict__ xs,
+                                                  const double* __restrict__ ws, int Ns,
+                                                  double* __restrict__ out, KParams kp, int self_omit) {
+    using K = Kern<KER>;
+    constexpr int M = K::M, NP = K::P;
+    __shared__ double sx[kTile], sy[kTile], sz[kTile], sw[M][kTile];
+    const int i = blockIdx.x * kTile + threadIdx.x;
+    const bool valid = i < Nt;
+    double x = 0, y = 0, z = 0;
+    if (valid) {
+        x = xt[3 * (size_t)i];
+        y = xt[3 * (size_t)i + 1];
+        z = xt[3 * (size_t)i + 2];
+    }
+    double tot[NP];
+#pragma unroll
+    for (int c = 0; c < NP; ++c) tot[c] = 0.0;
+    for (int tile = 0; tile < Ns; tile += kTile) {
+        const int j = tile + threadIdx.x;
+        if (j < Ns) {
+            sx[threadIdx.x] = xs[3 * (size_t)j];
+            sy[threadIdx.x] = xs[3 * (size_t)j + 1];
+            sz[threadIdx.x] = xs[3 * (size_t)j + 2];
+#pragma unroll
+            for (int m = 0; m < M; ++m) sw[m][threadIdx.x] = ws[(size_t)j * M + m];
+        }
+        __syncthreads();
+        const int cnt = min(kTile, Ns - tile);
+        double part[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) part[c] = 0.0;
+        for (int jj = 0; jj < cnt; ++jj) {
+            const double dx = x - sx[jj], dy = y - sy[jj], dz = z - sz[jj];
+            double f[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) f[m] = sw[m][jj];
+            const double s = fma(dx, dx, fma(dy, dy, fma(dz, dz, kp.e2)));
+            if (!self_omit || tile + jj != i) K::pair(dx, dy, dz, s, f, part, kp);
+        }
+#pragma unroll
+        for (int c = 0; c < NP; ++c) tot[c] += part[c];
+        __syncthreads();
+    }
+    if (valid)
+#pragma unroll
+        for (int c = 0; c < NP; ++c) out[(size_t)i * NP + c] = tot[c] * K::scale(c);
+}
+
+constexpr int kErrBlocks = 592;  // 4 x 148 SMs; fixed -> deterministic
+
+__global__ void __launch_bounds__(256) k_relerr(const double* __restrict__ ref, const double* __restrict__ ap,
+                                                long long n, double* __restrict__ part) {
+    double num = 0.0, den = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)kErrBlocks * 256) {
+        const double r = ref[i], d = r - ap[i];
+        num = fma(d, d, num);
+        den = fma(r, r, den);
+    }
+    __shared__ double sn[256], sd[256];
+    sn[threadIdx.x] = num;
+    sd[threadIdx.x] = den;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) {
+            sn[threadIdx.x] += sn[threadIdx.x + o];
+            sd[threadIdx.x] += sd[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = sn[0];
+        part[2 * blockIdx.x + 1] = sd[0];
+    }
+}
+
+}  // namespace
+
+kitc_status direct(int kernel, double eps, int self, const double* xt, int64_t Nt, const double* xs,
+                   const double* ws, int64_t Ns, double* out, cudaStream_t s) {
+    if (Nt < 0 || Ns < 0 || Nt > 0x7fffffffLL || Ns > 0x7fffffffLL)
+        return set_error(KITC_EINVAL, "kitc_direct: size out of range");
+    if (!(eps >= 0.0) || !std::isfinite(eps)) return set_error(KITC_EINVAL, "kitc_direct: eps must be >= 0");
+    if (self != KITC_SELF_OMIT && self != KITC_SELF_INCLUDE) return set_error(KITC_EINVAL, "kitc_direct: bad self");
+    if (self == KITC_SELF_OMIT && (xt != xs || Nt != Ns))
+        return set_error(KITC_EINVAL, "kitc_direct: KITC_SELF_OMIT needs targets == sources");
+    if (eps == 0.0 && self != KITC_SELF_OMIT)
+        return set_error(KITC_EINVAL, "kitc_direct: eps = 0 requires KITC_SELF_OMIT");
+    if (Nt == 0) return KITC_OK;
+    if (!xt || !out || (Ns > 0 && (!xs || !ws))) return set_error(KITC_EINVAL, "kitc_direct: NULL buffer");
+    const KParams kp = make_kparams(eps);
+    const int grid = (int)((Nt + kTile - 1) / kTile);
+    const int so = self == KITC_SELF_OMIT;
+    switch (kernel) {
+        case KITC_STOKESLET: k_direct<0><<<grid, kTile, 0, s>>>(xt, (int)Nt, xs, ws, (int)Ns, out, kp, so); note_launch(); break;
+        case KITC_ROTLET: k_direct<1><<<grid, kTile, 0, s>>>(xt, (int)Nt, xs, ws, (int)Ns, out, kp, so); note_launch(); break;
+        case KITC_STOKESLET_ROTLET: k_direct<2><<<grid, kTile, 0, s>>>(xt, (int)Nt, xs, ws, (int)Ns, out, kp, so); note_launch(); break;
+        default: return set_error(KITC_EINVAL, "kitc_direct: unknown kernel");
+    }
+    KITC_CUDA(cudaGetLastError());
+    return KITC_OK;
+}
+
+kitc_status rel_error(const double* ref, const double* ap, int64_t n, double* E, cudaStream_t s) {
+    if (!ref || !ap || !E || n < 1) return set_error(KITC_EINVAL, "kitc_rel_error: bad arguments");
+    double* part = nullptr;
+    KITC_CUDA(cudaMallocAsync(&part, 2 * kErrBlocks * sizeof(double), s));
+    k_relerr<<<kErrBlocks, 256, 0, s>>>(ref, ap, n, part); note_launch();
+    std::vector<double> h(2 * kErrBlocks);
+    cudaError_t e1 = cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(part, s);
+    KITC_CUDA(e1);
+    KITC_CUDA(cudaStreamSynchronize(s));
+    long double num = 0.0L, den = 0.0L;
+    for (int b = 0; b < kErrBlocks; ++b) {
+        num += h[2 * b];
+        den += h[2 * b + 1];
+    }
+    if (den == 0.0L) return set_error(KITC_EINVAL, "kitc_rel_error: reference is identically zero");
+    *E = (double)sqrtl(num / den);
+    return KITC_OK;
+}
+
+}  // namespace kitc

@@ -1,0 +1,264 @@
+// eval.cu -- treecode evaluation (Algorithm 2 lines 7-17) on sm_100a.
+//
+// One warp = one batch of <= 32 consecutive sorted targets inside one leaf
+// (spatially coherent).  The warp walks the tree depth-first with an explicit
+// shared-memory stack of (cluster, lane mask) entries, so every lane keeps the
+// paper's PER-TARGET semantics: a lane stops descending below a cluster it
+// accepted; lanes that reject a cluster descend into its children.  At each
+// popped cluster:
+//   MAC   r^2 <= (theta^2) R^2, R^2 > 0   (RN intrinsics, no FMA; readings A4/A5)
+//   far   accepted lanes sum the kernel against the (n+1)^3 proxies s_k with the
+//         modified weights fhat_k (Eq. pc_approximation_3D);
+//         uniform (broadcast) loads of fhat, tensor-product reuse of dx, dy, dz
+//   near  rejecting lanes at a leaf sum over its particles directly
+//         (Eq. pc_interaction_3D), j == i skipped by index (reading A8)
+//   else  rejecting lanes push the children.
+// Outputs are scaled once and scattered to original order (out[perm[t]]).
+#include <algorithm>
+
+#include "kitc_internal.cuh"
+#include "pair.cuh"
+
+namespace kitc {
+
+namespace {
+
+constexpr int kWarps = 4;  // warps (batches) per CTA
+
+struct EvalArgs {
+    const double* x;
+    const double* y;
+    const double* z;
+    const int* perm;
+    const double* w;  // sorted weights, M planes of N
+    const double4* cr;
+    const int4* topo;
+    const double* grid;
+    const double* fhat;
+    const int* bstart;
+    const int* bcount;
+    double* out;
+    unsigned long long* stats;
+    long long bb, be;
+    int N;
+    int P;  // n + 1 (runtime copy)
+    int stack_cap;
+    int self_omit;
+    double tt;  // theta * theta (RN)
+    KParams kp;
+};
+
+template <int PT, int KER>
+__device__ __forceinline__ void far_field(double x, double y, double z, const double* __restrict__ g,
+                                          const double* __restrict__ F, double* acc, const KParams& kp, int Prt) {
+    using K = Kern<KER>;
+    constexpr int M = K::M;
+    if constexpr (PT > 0) {
+        constexpr int P = PT, P3 = P * P * P;
+        double dz[P], ez[P];
+#pragma unroll
+        for (int k3 = 0; k3 < P; ++k3) {
+            dz[k3] = z - __ldg(g + 2 * P + k3);
+            ez[k3] = fma(dz[k3], dz[k3], kp.e2);
+        }
+        for (int k1 = 0; k1 < P; ++k1) {
+            const double dx = x - __ldg(g + k1);
+            const double dx2 = dx * dx;
+            for (int k2 = 0; k2 < P; ++k2) {
+                const double dy = y - __ldg(g + P + k2);
+                const double pxy = fma(dy, dy, dx2);
+                const double* Fk = F + (k1 * P + k2) * P;
+#pragma unroll
+                for (int k3 = 0; k3 < P; ++k3) {
+                    double f[M];
+#pragma unroll
+                    for (int m = 0; m < M; ++m) f[m] = __ldg(Fk + m * P3 + k3);
+                    K::pair(dx, dy, dz[k3], pxy + ez[k3], f, acc, kp);
+                }
+            }
+        }
+    } else {
+        const int P = Prt, P3 = P * P * P;
+        for (int k1 = 0; k1 < P; ++k1) {
+            const double dx = x - __ldg(g + k1);
+            for (int k2 = 0; k2 < P; ++k2) {
+                const double dy = y - __ldg(g + P + k2);
+                const double pxy = fma(dy, dy, dx * dx);
+                const double* Fk = F + (k1 * P + k2) * P;
+                for (int k3 = 0; k3 < P; ++k3) {
+                    const double dz = z - __ldg(g + 2 * P + k3);
+                    double f[M];
+#pragma unroll
+                    for (int m = 0; m < M; ++m) f[m] = __ldg(Fk + m * P3 + k3);
+                    K::pair(dx, dy, dz, pxy + fma(dz, dz, kp.e2), f, acc, kp);
+                }
+            }
+        }
+    }
+}
+
+template <int KER>
+__device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e,
+                                           const EvalArgs& a, double* acc) {
+    using K = Kern<KER>;
+    constexpr int M = K::M;
+    for (int j = b; j < e; ++j) {
+        const double dx = x - __ldg(a.x + j), dy = y - __ldg(a.y + j), dz = z - __ldg(a.z + j);
+        double f[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) f[m] = __ldg(a.w + (size_t)m * a.N + j);
+        const double s = fma(dx, dx, fma(dy, dy, fma(dz, dz, a.kp.e2)));
+        if (j != t || !a.self_omit) K::pair(dx, dy, dz, s, f, acc, a.kp);
+    }
+}
+
+template <int PT, int KER>
+__global__ void __launch_bounds__(kWarps * 32) k_eval(const EvalArgs a) {
+    using K = Kern<KER>;
+    constexpr int M = K::M, NP = K::P;
+    extern __shared__ int2 smem_stack[];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    int2* stk = smem_stack + wl * a.stack_cap;
+    const long long b = a.bb + (long long)blockIdx.x * kWarps + wl;
+    if (b >= a.be) return;  // whole warp
+    const int t0 = a.bstart[b], tc = a.bcount[b];
+    const bool valid = lane < tc;
+    const int t = t0 + (valid ? lane : 0);
+    const double x = a.x[t], y = a.y[t], z = a.z[t];
+    const int P = PT > 0 ? PT : a.P;
+    const int P3 = P * P * P;
+    double acc[NP];
+#pragma unroll
+    for (int c = 0; c < NP; ++c) acc[c] = 0.0;
+    unsigned long long st[5] = {0, 0, 0, 0, 0};
+    const unsigned live = __ballot_sync(0xffffffffu, valid);
+    if (lane == 0) stk[0] = make_int2(0, (int)live);
+    __syncwarp();
+    int sp = 1;
+    while (sp > 0) {
+        --sp;
+        const int2 ent = stk[sp];
+        __syncwarp();
+        const int c = ent.x;
+        const unsigned mask = (unsigned)ent.y;
+        const bool in = (mask >> lane) & 1u;
+        const double4 cr = a.cr[c];
+        bool ok = false;
+        if (in) {
+            const double dx = __dsub_rn(x, cr.x), dy = __dsub_rn(y, cr.y), dz = __dsub_rn(z, cr.z);
+            const double R2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            ok = R2 > 0.0 && cr.w <= __dmul_rn(a.tt, R2);
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, ok);
+        const unsigned rm = mask & ~am;
+        const int4 tp = a.topo[c];
+        if (am && ok) {
+            far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * M * P3, acc, a.kp, P);
+            if (a.stats) {
+                st[0] += 1;
+                st[1] += (unsigned long long)P3;
+                st[4] += (unsigned long long)(tp.y - tp.x);
+            }
+        }
+        if (rm) {
+            if (tp.w == 0) {
+                if (in && !ok) {
+                    near_field<KER>(x, y, z, t, tp.x, tp.y, a, acc);
+                    if (a.stats) {
+                        const int self = (a.self_omit && t >= tp.x && t < tp.y) ? 1 : 0;
+                        st[2] += 1;
+                        st[3] += (unsigned long long)(tp.y - tp.x - self);
+                        st[4] += (unsigned long long)(tp.y - tp.x);
+                    }
+                }
+            } else {
+                // children pushed in reverse so the first child is popped first (A17)
+                if (lane < tp.w) stk[sp + tp.w - 1 - lane] = make_int2(tp.z + lane, (int)rm);
+                sp += tp.w;
+                __syncwarp();
+            }
+        }
+    }
+    if (!valid) return;
+    const int o = a.perm[t];
+#pragma unroll
+    for (int c = 0; c < NP; ++c) a.out[(size_t)o * NP + c] = acc[c] * K::scale(c);
+    if (a.stats)
+        for (int k = 0; k < 5; ++k) a.stats[(size_t)o * 5 + k] = st[k];
+}
+
+template <int PT, int KER>
+static void launch(const EvalArgs& a, int grid, size_t smem, cudaStream_t s) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_eval<PT, KER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_eval<PT, KER><<<grid, kWarps * 32, smem, s>>>(a); note_launch();
+}
+
+template <int KER>
+static void dispatch(int P, const EvalArgs& a, int grid, size_t smem, cudaStream_t s) {
+    switch (P) {
+        case 2: launch<2, KER>(a, grid, smem, s); break;
+        case 3: launch<3, KER>(a, grid, smem, s); break;
+        case 4: launch<4, KER>(a, grid, smem, s); break;
+        case 5: launch<5, KER>(a, grid, smem, s); break;
+        case 6: launch<6, KER>(a, grid, smem, s); break;
+        case 7: launch<7, KER>(a, grid, smem, s); break;
+        case 8: launch<8, KER>(a, grid, smem, s); break;
+        case 9: launch<9, KER>(a, grid, smem, s); break;
+        case 10: launch<10, KER>(a, grid, smem, s); break;
+        case 11: launch<11, KER>(a, grid, smem, s); break;
+        default: launch<0, KER>(a, grid, smem, s); break;
+    }
+}
+
+}  // namespace
+
+kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps, int self, const double* fhat,
+                 int64_t bb, int64_t be, double* out, uint64_t* stats, cudaStream_t s) {
+    if (!t->built) return set_error(KITC_ESTATE, "kitc_eval: tree not built");
+    if (!t->weights_ready || t->grid_n != n || t->weights_kernel != kernel)
+        return set_error(KITC_ESTATE, "kitc_eval: call kitc_modified_weights with the same kernel and n first");
+    if (!(theta >= 0.0 && theta < 1.0)) return set_error(KITC_EINVAL, "kitc_eval: theta must be in [0, 1)");
+    if (!(eps >= 0.0) || !std::isfinite(eps)) return set_error(KITC_EINVAL, "kitc_eval: eps must be >= 0");
+    if (self != KITC_SELF_OMIT && self != KITC_SELF_INCLUDE) return set_error(KITC_EINVAL, "kitc_eval: bad self");
+    if (eps == 0.0 && self != KITC_SELF_OMIT)
+        return set_error(KITC_EINVAL, "kitc_eval: eps = 0 requires KITC_SELF_OMIT (singular kernel)");
+    if (bb < 0 || be > t->nbatches || bb > be) return set_error(KITC_EINVAL, "kitc_eval: bad batch range");
+    if (!fhat || !out) return set_error(KITC_EINVAL, "kitc_eval: NULL buffer");
+    if (be == bb) return KITC_OK;
+    EvalArgs a;
+    a.x = t->x.as<double>();
+    a.y = t->y.as<double>();
+    a.z = t->z.as<double>();
+    a.perm = t->perm.as<int>();
+    a.w = t->w.as<double>();
+    a.cr = t->cr.as<double4>();
+    a.topo = t->topo.as<int4>();
+    a.grid = t->grid.as<double>();
+    a.fhat = fhat;
+    a.bstart = t->bstart.as<int>();
+    a.bcount = t->bcount.as<int>();
+    a.out = out;
+    a.stats = reinterpret_cast<unsigned long long*>(stats);
+    a.bb = bb;
+    a.be = be;
+    a.N = (int)t->N;
+    a.P = n + 1;
+    a.stack_cap = 8 * (t->depth + 1);
+    a.self_omit = self == KITC_SELF_OMIT;
+    a.tt = theta * theta;
+    a.kp = make_kparams(eps);
+    const size_t smem = (size_t)kWarps * a.stack_cap * sizeof(int2);
+    if (smem > 200 * 1024) return set_error(KITC_EINVAL, "kitc_eval: tree too deep for the traversal stack");
+    const long long nb = be - bb;
+    const int grid = (int)((nb + kWarps - 1) / kWarps);
+    switch (kernel) {
+        case KITC_STOKESLET: dispatch<0>(n + 1, a, grid, smem, s); break;
+        case KITC_ROTLET: dispatch<1>(n + 1, a, grid, smem, s); break;
+        case KITC_STOKESLET_ROTLET: dispatch<2>(n + 1, a, grid, smem, s); break;
+        default: return set_error(KITC_EINVAL, "kitc_eval: unknown kernel");
+    }
+    KITC_CUDA(cudaGetLastError());
+    return KITC_OK;
+}
+
+}  // namespace kitc

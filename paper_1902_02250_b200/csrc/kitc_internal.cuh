@@ -1,0 +1,106 @@
+// kitc_internal.cuh -- shared internals of libkitc.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "../../include/kitc.h"
+
+namespace kitc {
+
+constexpr int kMaxDegree = 16;        // n in [1, 16]
+constexpr int kBatch = 32;            // targets per warp batch
+constexpr double kPi = 3.14159265358979323846;
+
+extern std::atomic<unsigned long long> g_launches;  // kernels launched by the library
+inline void note_launch(unsigned long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ---- error plumbing ---------------------------------------------------------
+kitc_status set_error(kitc_status st, const std::string& msg);
+kitc_status check_cuda(cudaError_t e, const char* what);
+#define KITC_TRY(expr)                                   \
+    do {                                                 \
+        kitc_status _st = (expr);                        \
+        if (_st != KITC_OK) return _st;                  \
+    } while (0)
+#define KITC_CUDA(expr) KITC_TRY(::kitc::check_cuda((expr), #expr))
+
+// Stream-ordered device buffer, grown on demand, retained across rebuilds.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    kitc_status ensure(size_t need, cudaStream_t s, bool keep = false);
+    void release(cudaStream_t s);
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Pinned host staging buffer.
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    kitc_status ensure(size_t need);
+    void release();
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace kitc
+
+// The opaque handle.
+struct kitc_tree {
+    cudaStream_t stream = nullptr;  // stream of the last build (for frees)
+    int64_t N = 0;
+    int32_t N0 = 0;
+    int32_t depth = 0;
+    int32_t ndegenerate = 0;
+    int64_t nclusters = 0;
+    int64_t nbatches = 0;
+    bool built = false;
+
+    // sorted particles (SoA)
+    kitc::DevBuf x, y, z, perm;          // double x3, int32
+    kitc::DevBuf x2, y2, z2, perm2;      // partition scratch
+    kitc::DevBuf w;                      // sorted weights, m planes of N doubles
+    int32_t w_m = 0;
+    bool weights_ready = false;
+    int32_t grid_n = -1;                 // degree of the stored grids
+    int32_t weights_kernel = -1;
+
+    // clusters
+    kitc::DevBuf box;    // double[C][6]  lo xyz, hi xyz
+    kitc::DevBuf cr;     // double4[C]    centre xyz, r^2
+    kitc::DevBuf topo;   // int4[C]       begin, end, first_child, nchild
+    kitc::DevBuf grid;   // double[C][3][n+1]
+    kitc::DevBuf bstart; // int32[nbatches] first target of the batch (sorted index)
+    kitc::DevBuf bcount; // int32[nbatches]
+
+    // host mirrors of the topology
+    std::vector<int32_t> h_begin, h_end, h_level, h_parent, h_first, h_nchild;
+    std::vector<int32_t> h_bstart, h_bcount;
+    std::vector<int64_t> h_bprefix;      // targets in batches [0, b)
+
+    // build scratch
+    kitc::DevBuf d_items, d_part, d_cnt, d_off, d_lvl, d_split, d_flag;
+    kitc::HostBuf h_stage, h_cnt;
+    // weights scratch
+    kitc::DevBuf d_witems, d_wpart;
+};
+
+namespace kitc {
+// tree.cu
+kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N, int32_t N0, cudaStream_t s);
+// weights.cu
+kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, int64_t cb,
+                             int64_t ce, double* fhat, cudaStream_t s);
+// eval.cu
+kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps, int self,
+                 const double* fhat, int64_t bb, int64_t be, double* out, uint64_t* stats,
+                 cudaStream_t s);
+// direct.cu
+kitc_status direct(int kernel, double eps, int self, const double* xt, int64_t Nt,
+                   const double* xs, const double* ws, int64_t Ns, double* out, cudaStream_t s);
+kitc_status rel_error(const double* ref, const double* approx, int64_t count, double* E,
+                      cudaStream_t s);
+}  // namespace kitc

@@ -1,0 +1,121 @@
+// pair.cuh -- the MRS pair terms on CUDA cores (fp64), §7.
+//
+// With d = x - y, s = |d|^2 + eps^2 and rs = s^{-1/2} (hardware rsqrt seed +
+// Newton, 1 ulp), the scalar functions of Eq. MRS_kernels are
+//   8 pi H1 = (2 eps^2 + r^2) s^{-3/2} = rs + eps^2 rs^3
+//   8 pi H2 = rs^3
+//   8 pi Q  = (5 eps^2 + 2 r^2) s^{-5/2} = 2 rs^3 + 3 eps^2 rs^5
+//   8 pi D1 = (10 eps^4 - 7 eps^2 r^2 - 2 r^4) s^{-7/2} = 15 eps^4 rs^7 - 3 eps^2 rs^5 - 2 rs^3
+//   8 pi D2 = (21 eps^2 + 6 r^2) s^{-7/2} = 6 rs^5 + 15 eps^2 rs^7
+// (substitute r^2 = s - eps^2).  Constants 1/(8 pi), 1/2, 1/4 are applied once
+// per target at the end (scale()).  These differ from the literal formulas by
+// rounding only.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace kitc {
+
+struct KParams {
+    double e2;      // eps^2
+    double e2x3;    // 3 eps^2
+    double e4x15;   // 15 eps^4
+    double e2x15;   // 15 eps^2
+};
+
+template <int KER> struct Kern;
+
+// Stokeslet, Eq. Velocity_1: u = f H1 + [f.d] d H2.   m = 3, p = 3
+template <> struct Kern<0> {
+    static constexpr int M = 3, P = 3;
+    static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s,
+                                                const double* f, double* acc, const KParams& k) {
+        double rs = rsqrt(s);
+        double rs2 = rs * rs;
+        double rs3 = rs2 * rs;
+        double h1 = fma(k.e2, rs3, rs);
+        double fd = fma(f[0], dx, fma(f[1], dy, f[2] * dz));
+        double c = fd * rs3;
+        acc[0] = fma(c, dx, fma(f[0], h1, acc[0]));
+        acc[1] = fma(c, dy, fma(f[1], h1, acc[1]));
+        acc[2] = fma(c, dz, fma(f[2], h1, acc[2]));
+    }
+    // 1/(8 pi)
+    static __device__ __forceinline__ double scale(int) { return 1.0 / (8.0 * 3.14159265358979323846); }
+};
+
+// Rotlet (Eqs. Velocity_2 / AngularVelocity with f = 0; readings A9, A10):
+//   u = 1/2 [g x d] Q,   w = 1/4 g D1 + 1/4 [g.d] d D2.     m = 3, p = 6
+template <> struct Kern<1> {
+    static constexpr int M = 3, P = 6;
+    static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s,
+                                                const double* g, double* acc, const KParams& k) {
+        double rs = rsqrt(s);
+        double rs2 = rs * rs;
+        double rs3 = rs2 * rs;
+        double rs5 = rs3 * rs2;
+        double rs7 = rs5 * rs2;
+        double q = fma(k.e2x3, rs5, 2.0 * rs3);
+        double d1 = fma(k.e4x15, rs7, -q);   // 8 pi D1 = 15 eps^4 rs^7 - 8 pi Q
+        double d2 = fma(k.e2x15, rs7, 6.0 * rs5);
+        double cx = g[1] * dz - g[2] * dy;
+        double cy = g[2] * dx - g[0] * dz;
+        double cz = g[0] * dy - g[1] * dx;
+        acc[0] = fma(cx, q, acc[0]);
+        acc[1] = fma(cy, q, acc[1]);
+        acc[2] = fma(cz, q, acc[2]);
+        double gd = fma(g[0], dx, fma(g[1], dy, g[2] * dz)) * d2;
+        acc[3] = fma(gd, dx, fma(g[0], d1, acc[3]));
+        acc[4] = fma(gd, dy, fma(g[1], d1, acc[4]));
+        acc[5] = fma(gd, dz, fma(g[2], d1, acc[5]));
+    }
+    // u: 1/(16 pi), w: 1/(32 pi)
+    static __device__ __forceinline__ double scale(int c) {
+        return c < 3 ? 1.0 / (16.0 * 3.14159265358979323846) : 1.0 / (32.0 * 3.14159265358979323846);
+    }
+};
+
+// Stokeslet + rotlet (Eqs. Velocity_2 / AngularVelocity), weights (f, n):
+//   u = f H1 + [f.d] d H2 + 1/2 [n x d] Q,  w = 1/2 [f x d] Q + 1/4 n D1 + 1/4 [n.d] d D2
+// accumulated as 16 pi u and 32 pi w.                          m = 6, p = 6
+template <> struct Kern<2> {
+    static constexpr int M = 6, P = 6;
+    static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s,
+                                                const double* f, double* acc, const KParams& k) {
+        double rs = rsqrt(s);
+        double rs2 = rs * rs;
+        double rs3 = rs2 * rs;
+        double rs5 = rs3 * rs2;
+        double rs7 = rs5 * rs2;
+        double h1x2 = 2.0 * fma(k.e2, rs3, rs);
+        double q = fma(k.e2x3, rs5, 2.0 * rs3);
+        double d1 = fma(k.e4x15, rs7, -q);   // 8 pi D1 = 15 eps^4 rs^7 - 8 pi Q
+        double d2 = fma(k.e2x15, rs7, 6.0 * rs5);
+        const double* g = f + 3;
+        double fd2 = 2.0 * fma(f[0], dx, fma(f[1], dy, f[2] * dz)) * rs3;
+        double nx = g[1] * dz - g[2] * dy, ny = g[2] * dx - g[0] * dz, nz = g[0] * dy - g[1] * dx;
+        acc[0] = fma(nx, q, fma(fd2, dx, fma(f[0], h1x2, acc[0])));
+        acc[1] = fma(ny, q, fma(fd2, dy, fma(f[1], h1x2, acc[1])));
+        acc[2] = fma(nz, q, fma(fd2, dz, fma(f[2], h1x2, acc[2])));
+        double fx = f[1] * dz - f[2] * dy, fy = f[2] * dx - f[0] * dz, fz = f[0] * dy - f[1] * dx;
+        double q2 = 2.0 * q;
+        double gd = fma(g[0], dx, fma(g[1], dy, g[2] * dz)) * d2;
+        acc[3] = fma(fx, q2, fma(gd, dx, fma(g[0], d1, acc[3])));
+        acc[4] = fma(fy, q2, fma(gd, dy, fma(g[1], d1, acc[4])));
+        acc[5] = fma(fz, q2, fma(gd, dz, fma(g[2], d1, acc[5])));
+    }
+    static __device__ __forceinline__ double scale(int c) {
+        return c < 3 ? 1.0 / (16.0 * 3.14159265358979323846) : 1.0 / (32.0 * 3.14159265358979323846);
+    }
+};
+
+inline KParams make_kparams(double eps) {
+    KParams k;
+    double e2 = eps * eps;
+    k.e2 = e2;
+    k.e2x3 = 3.0 * e2;
+    k.e4x15 = 15.0 * e2 * e2;
+    k.e2x15 = 15.0 * e2;
+    return k;
+}
+
+}  // namespace kitc

@@ -1,0 +1,237 @@
+// weights.cu -- modified weights (Eq. modified_weights, Algorithm 1
+// P:528-557) as an sm_100a fp64 kernel.
+//
+// Work item = (cluster, chunk of <= kChunk of its particles).  Per tile of kTile
+// particles, phase 1 forms the three per-axis barycentric vectors
+//   L_l,k = a_k / sum_k' a_k',  a_k = w_k / (y_l - s_l,k)       (Eq. Barycentric-1D)
+// with the DBL_MIN coincidence flag (Algorithm 1 lines 10, 15-17: L = e_flag,
+// last k wins) and stages them with the weights in shared memory; phase 2 has
+// thread (k2, k3) accumulate fhat[m][k1][k2][k3] += Lx[k1] (Ly[k2] Lz[k3] f_m)
+// in registers for all k1 and m (the tensor-product loop of lines 20-22).
+// Chunks of one cluster write partials that a second kernel sums in chunk
+// order (deterministic).  Reading A15: L per axis instead of
+// (a1 a2 a3 / denom) -- rounding-only difference.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+
+#include "kitc_internal.cuh"
+
+namespace kitc {
+
+namespace {
+
+constexpr int kChunk = 4096;  // particles per work item
+constexpr int kTile = 64;     // particles staged per shared-memory tile
+
+struct WItem {
+    int32_t c;     // cluster id
+    int32_t b, e;  // particle range (sorted indices)
+    int32_t slot;  // -1: write fhat directly; >= 0: partial slot
+};
+
+struct Nodes {
+    double t[kMaxDegree + 1];
+};
+
+__global__ void k_gather_w(const double* __restrict__ w, const int* __restrict__ perm, int N, int m,
+                           double* __restrict__ ws) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const size_t o = (size_t)perm[i] * m;
+    for (int c = 0; c < m; ++c) ws[(size_t)c * N + i] = w[o + c];
+}
+
+// grid s_{l,k} = c_l + h_l t_k, s_{l,0} = hi_l, s_{l,n} = lo_l (reading A13), RN.
+__global__ void k_grids(int C, int n, Nodes nd, const double* __restrict__ box, double* __restrict__ grid) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const int P = n + 1;
+    for (int l = 0; l < 3; ++l) {
+        const double lo = box[(size_t)c * 6 + l], hi = box[(size_t)c * 6 + 3 + l];
+        const double ctr = __dmul_rn(0.5, __dadd_rn(lo, hi)), h = __dmul_rn(0.5, __dsub_rn(hi, lo));
+        double* g = grid + ((size_t)c * 3 + l) * P;
+        for (int k = 0; k <= n; ++k) g[k] = __dadd_rn(ctr, __dmul_rn(h, nd.t[k]));
+        g[0] = hi;
+        g[n] = lo;
+    }
+}
+
+// 1D barycentric vector of coordinate v on nodes s (Algorithm 1 lines 9-17).
+template <int P>
+__device__ __forceinline__ void bary(double v, const double* s, double* L) {
+    double sum = 0.0;
+    int flag = -1;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const double diff = v - s[k];
+        const double wk = (k == 0 || k == P - 1) ? ((k & 1) ? -0.5 : 0.5) : ((k & 1) ? -1.0 : 1.0);
+        if (fabs(diff) <= DBL_MIN) {
+            flag = k;
+            L[k] = 0.0;
+        } else {
+            L[k] = wk / diff;
+            sum += L[k];
+        }
+    }
+    if (flag >= 0) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) L[k] = (k == flag) ? 1.0 : 0.0;
+    } else {
+        const double inv = 1.0 / sum;
+#pragma unroll
+        for (int k = 0; k < P; ++k) L[k] *= inv;
+    }
+}
+
+template <int P, int M>
+__global__ void __launch_bounds__((P * P + 31) / 32 * 32) k_weights(
+    const WItem* __restrict__ items, const double* __restrict__ x, const double* __restrict__ y,
+    const double* __restrict__ z, const double* __restrict__ ws, int N, const double* __restrict__ grid,
+    double* __restrict__ fhat, double* __restrict__ part) {
+    constexpr int P2 = P * P, P3 = P2 * P, NT = (P2 + 31) / 32 * 32;
+    __shared__ double sg[3 * P];
+    __shared__ double Lx[kTile][P], Ly[kTile][P], Lz[kTile][P], sw[kTile][M];
+    const WItem it = items[blockIdx.x];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 3 * P; i += NT) sg[i] = grid[(size_t)it.c * 3 * P + i];
+    const int k2 = tid / P, k3 = tid % P;
+    const bool owner = tid < P2;
+    double acc[M][P];
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int k = 0; k < P; ++k) acc[m][k] = 0.0;
+    __syncthreads();
+    for (int tile = it.b; tile < it.e; tile += kTile) {
+        const int cnt = min(kTile, it.e - tile);
+        for (int j = tid; j < cnt; j += NT) {
+            const int i = tile + j;
+            bary<P>(x[i], sg, Lx[j]);
+            bary<P>(y[i], sg + P, Ly[j]);
+            bary<P>(z[i], sg + 2 * P, Lz[j]);
+#pragma unroll
+            for (int m = 0; m < M; ++m) sw[j][m] = ws[(size_t)m * N + i];
+        }
+        __syncthreads();
+        if (owner) {
+            for (int j = 0; j < cnt; ++j) {
+                const double q = Ly[j][k2] * Lz[j][k3];
+#pragma unroll
+                for (int m = 0; m < M; ++m) {
+                    const double g = q * sw[j][m];
+#pragma unroll
+                    for (int k1 = 0; k1 < P; ++k1) acc[m][k1] = fma(Lx[j][k1], g, acc[m][k1]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (!owner) return;
+    double* dst = it.slot < 0 ? fhat + (size_t)it.c * M * P3 : part + (size_t)it.slot * M * P3;
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) dst[m * P3 + k1 * P2 + tid] = acc[m][k1];
+}
+
+struct RItem {
+    int32_t c, first_slot, nslots, pad;
+};
+
+// fhat[c] = sum of its partial slots in chunk order (deterministic).
+__global__ void k_reduce(const RItem* __restrict__ r, int len, const double* __restrict__ part,
+                         double* __restrict__ fhat) {
+    const RItem it = r[blockIdx.x];
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        double s = part[(size_t)it.first_slot * len + i];
+        for (int k = 1; k < it.nslots; ++k) s += part[(size_t)(it.first_slot + k) * len + i];
+        fhat[(size_t)it.c * len + i] = s;
+    }
+}
+
+template <int P, int M>
+static void launch_weights(int nitems, const WItem* items, const kitc_tree* t, const double* ws,
+                           const double* grid, double* fhat, double* part, cudaStream_t s) {
+    constexpr int NT = (P * P + 31) / 32 * 32;
+    k_weights<P, M><<<nitems, NT, 0, s>>>(items, t->x.as<double>(), t->y.as<double>(), t->z.as<double>(), ws,
+                                          (int)t->N, grid, fhat, part); note_launch();
+}
+
+template <int M>
+static kitc_status dispatch(int n, int nitems, const WItem* items, const kitc_tree* t, const double* ws,
+                            const double* grid, double* fhat, double* part, cudaStream_t s) {
+    switch (n + 1) {
+#define KITC_W(P) \
+    case P: launch_weights<P, M>(nitems, items, t, ws, grid, fhat, part, s); break;
+        KITC_W(2) KITC_W(3) KITC_W(4) KITC_W(5) KITC_W(6) KITC_W(7) KITC_W(8) KITC_W(9) KITC_W(10)
+        KITC_W(11) KITC_W(12) KITC_W(13) KITC_W(14) KITC_W(15) KITC_W(16) KITC_W(17)
+#undef KITC_W
+        default: return set_error(KITC_EINVAL, "kitc_modified_weights: n out of range");
+    }
+    return KITC_OK;
+}
+
+}  // namespace
+
+kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, int64_t cb, int64_t ce,
+                             double* fhat, cudaStream_t s) {
+    int32_t m = 0, p = 0;
+    KITC_TRY(kitc_kernel_dims(kernel, &m, &p));
+    if (n < 1 || n > kMaxDegree) return set_error(KITC_EINVAL, "kitc_modified_weights: n must be in [1, 16]");
+    if (!t->built) return set_error(KITC_ESTATE, "kitc_modified_weights: tree not built");
+    if (cb < 0 || ce > t->nclusters || cb > ce) return set_error(KITC_EINVAL, "kitc_modified_weights: bad cluster range");
+    if (!w || (!fhat && ce > cb)) return set_error(KITC_EINVAL, "kitc_modified_weights: NULL buffer");
+    const int N = (int)t->N, C = (int)t->nclusters, P = n + 1, P3 = P * P * P;
+    // sorted weights (SoA, m planes)
+    KITC_TRY(t->w.ensure((size_t)m * N * sizeof(double), s));
+    k_gather_w<<<(N + 255) / 256, 256, 0, s>>>(w, t->perm.as<int>(), N, m, t->w.as<double>()); note_launch();
+    // grids of every cluster (reading A12: t_k = sin(pi (n - 2k) / (2n)))
+    Nodes nd;
+    for (int k = 0; k <= n; ++k) nd.t[k] = std::sin(kPi * (double)(n - 2 * k) / (2.0 * (double)n));
+    KITC_TRY(t->grid.ensure((size_t)C * 3 * P * sizeof(double), s));
+    k_grids<<<(C + 127) / 128, 128, 0, s>>>(C, n, nd, t->box.as<double>(), t->grid.as<double>()); note_launch();
+    KITC_CUDA(cudaGetLastError());
+    t->w_m = m;
+    t->grid_n = n;
+    t->weights_kernel = kernel;
+    t->weights_ready = true;
+    if (ce == cb) return KITC_OK;
+    // work items
+    std::vector<WItem> items;
+    std::vector<RItem> red;
+    int nslots = 0;
+    for (int64_t c = cb; c < ce; ++c) {
+        const int b = t->h_begin[c], e = t->h_end[c];
+        const int nch = (e - b + kChunk - 1) / kChunk;
+        if (nch == 1) {
+            items.push_back(WItem{(int)c, b, e, -1});
+        } else {
+            red.push_back(RItem{(int)c, nslots, nch, 0});
+            for (int q = 0; q < nch; ++q)
+                items.push_back(WItem{(int)c, b + q * kChunk, std::min(e, b + (q + 1) * kChunk), nslots++});
+        }
+    }
+    const size_t o1 = (items.size() * sizeof(WItem) + 15) / 16 * 16, o2 = o1 + red.size() * sizeof(RItem);
+    KITC_CUDA(cudaStreamSynchronize(s));  // staging buffer reuse
+    KITC_TRY(t->h_stage.ensure(o2));
+    std::copy(items.begin(), items.end(), t->h_stage.as<WItem>());
+    std::copy(red.begin(), red.end(), reinterpret_cast<RItem*>(t->h_stage.as<char>() + o1));
+    KITC_TRY(t->d_witems.ensure(o2, s));
+    KITC_CUDA(cudaMemcpyAsync(t->d_witems.p, t->h_stage.p, o2, cudaMemcpyHostToDevice, s));
+    KITC_TRY(t->d_wpart.ensure((size_t)std::max(nslots, 1) * m * P3 * sizeof(double), s));
+    const WItem* di = t->d_witems.as<WItem>();
+    if (m == 3)
+        KITC_TRY(dispatch<3>(n, (int)items.size(), di, t, t->w.as<double>(), t->grid.as<double>(), fhat,
+                             t->d_wpart.as<double>(), s));
+    else
+        KITC_TRY(dispatch<6>(n, (int)items.size(), di, t, t->w.as<double>(), t->grid.as<double>(), fhat,
+                             t->d_wpart.as<double>(), s));
+    if (!red.empty())
+        k_reduce<<<(int)red.size(), 256, 0, s>>>(reinterpret_cast<const RItem*>(t->d_witems.as<char>() + o1),
+                                                 m * P3, t->d_wpart.as<double>(), fhat); note_launch();
+    KITC_CUDA(cudaGetLastError());
+    return KITC_OK;
+}
+
+}  // namespace kitc

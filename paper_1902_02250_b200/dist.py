@@ -1,0 +1,63 @@
+"""Multi-GPU plumbing for the KITC hot path (one process per GPU, torch.distributed).
+
+Decomposition:
+  * every rank builds the same tree redundantly (deterministic, bit-exact);
+  * modified weights are SHARDED: rank r computes clusters [cb_r, ce_r),
+    contiguous ranges balanced by sum of N_C (Algorithm 1 costs O(n^3 N_C));
+  * ONE exchange step: an NCCL all-gather replicates fhat over NVLink (shards
+    padded to equal size, gathered in place, then placed at their cluster
+    offsets with device-to-device copies);
+  * targets are partitioned by 32-target batches, contiguous ranges balanced
+    by target count; outputs stay sharded (each rank writes its targets).
+Per-target traversal and summation orders do not depend on the partition, so
+outputs are bitwise identical for any number of ranks.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def balanced_ranges(weights, k, start=0):
+    """Split items [start, len(weights)) into k contiguous ranges with roughly
+    equal sum of weights.  Returns [(b, e)] (possibly empty ranges)."""
+    w = np.asarray(weights[start:], dtype=np.float64)
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    tot = cum[-1]
+    cuts = [start]
+    for r in range(1, k):
+        cuts.append(start + int(np.searchsorted(cum, tot * r / k, side="left")))
+    cuts.append(len(weights))
+    for i in range(1, len(cuts)):
+        cuts[i] = max(cuts[i], cuts[i - 1])
+    return [(cuts[i], cuts[i + 1]) for i in range(k)]
+
+
+def cluster_shards(begin, end, k, skip_root=True):
+    """Cluster ranges per rank, balanced by N_C.  skip_root: with targets =
+    sources and theta < 1 the root is never accepted (every target lies in
+    its box, R <= r), so its fhat is never read (reading A16)."""
+    sizes = np.asarray(end) - np.asarray(begin)
+    return balanced_ranges(sizes, k, start=1 if (skip_root and len(sizes) > 1) else 0)
+
+
+def batch_shards(batch_prefix, k):
+    """Batch ranges per rank balanced by target count; batch_prefix[b] =
+    targets in batches [0, b) (length nbatches + 1)."""
+    counts = np.diff(np.asarray(batch_prefix))
+    return balanced_ranges(counts, k)
+
+
+def padded_shard_size(shards):
+    return max(1, max(e - b for b, e in shards))
+
+
+def all_gather_fhat(fhat_full, gathered, shard, shards, rank, group=None):
+    """Replicate fhat: `shard` (= gathered[rank]) holds this rank's clusters;
+    all-gather in place into `gathered` [k, S, ...], then copy each rank's
+    valid clusters to their offsets in `fhat_full`."""
+    import torch.distributed as dist
+    dist.all_gather_into_tensor(gathered.view(-1), shard.reshape(-1), group=group)
+    for r, (b, e) in enumerate(shards):
+        if e > b:
+            fhat_full[b:e].copy_(gathered[r, : e - b])
+    return fhat_full

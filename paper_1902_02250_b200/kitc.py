@@ -1,0 +1,273 @@
+"""Python binding of libkitc.so (include/kitc.h) -- argument marshalling only.
+
+Every step of the KITC path runs in the library's CUDA kernels; this module
+passes pointers, sizes and the current CUDA stream through ctypes, and uses
+PyTorch only for device memory and streams.  There is NO CPU fallback: if
+libkitc.so is missing or fails to load, importing this module raises.
+
+Raw entry points carry the C names (kitc_build_tree, kitc_modified_weights,
+kitc_eval, kitc_direct, ...).  `Tree` and `treecode()` are the convenience
+layer: `treecode(X, W, kernel, n, theta, N0, eps)` is the one-shot
+``eval(kernel, n, theta, N0, eps)`` of the north star, chaining
+build_tree -> modified_weights -> eval.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkitc.so")
+
+KITC_OK, KITC_EINVAL, KITC_ENOMEM, KITC_ECUDA, KITC_ESTATE = 0, -1, -2, -3, -4
+STOKESLET, ROTLET, STOKESLET_ROTLET = 0, 1, 2
+SELF_OMIT, SELF_INCLUDE = 0, 1
+KERNELS = {"stokeslet": STOKESLET, "rotlet": ROTLET, "stokeslet_rotlet": STOKESLET_ROTLET}
+
+# every symbol include/kitc.h declares
+EXPORTS = ("kitc_kernel_dims", "kitc_tree_create", "kitc_build_tree", "kitc_tree_info",
+           "kitc_tree_export", "kitc_modified_weights", "kitc_eval", "kitc_batch_targets",
+           "kitc_direct", "kitc_rel_error", "kitc_tree_free", "kitc_last_error",
+           "kitc_launch_count")
+
+
+class KitcError(RuntimeError):
+    def __init__(self, fn, status, msg):
+        super().__init__(f"{fn} failed with status {status}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libkitc.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    i32, i64, d, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
+    P = C.POINTER
+    sig = {
+        "kitc_kernel_dims": [i32, P(i32), P(i32)],
+        "kitc_tree_create": [P(vp)],
+        "kitc_build_tree": [vp, vp, i64, i32, vp],
+        "kitc_tree_info": [vp, P(i64), P(i32), P(i64), P(i32)],
+        "kitc_tree_export": [vp] + [vp] * 9,
+        "kitc_modified_weights": [vp, i32, i32, vp, i64, i64, vp, vp],
+        "kitc_eval": [vp, i32, i32, d, i32, d, i32, vp, i64, i64, vp, vp, vp],
+        "kitc_batch_targets": [vp, i64, P(i64)],
+        "kitc_direct": [i32, d, i32, vp, i64, vp, vp, i64, vp, vp],
+        "kitc_rel_error": [vp, vp, i64, P(d), vp],
+        "kitc_tree_free": [vp],
+        "kitc_last_error": [],
+        "kitc_launch_count": [],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = C.c_int32
+    L.kitc_tree_free.restype = None
+    L.kitc_last_error.restype = C.c_char_p
+    L.kitc_launch_count.restype = C.c_uint64
+    return L
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _call(name, *args):
+    st = getattr(_lib, name)(*args)
+    if st != KITC_OK:
+        raise KitcError(name, st, _lib.kitc_last_error().decode())
+    return st
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _dev_f64(t, shape1):
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    if t.dim() != 2 or t.shape[1] != shape1:
+        raise ValueError(f"expected shape [N, {shape1}], got {tuple(t.shape)}")
+    return t
+
+
+# ---- raw C entry points (same names as include/kitc.h) -----------------------
+
+def kitc_kernel_dims(kernel):
+    m, p = C.c_int32(), C.c_int32()
+    _call("kitc_kernel_dims", int(kernel), C.byref(m), C.byref(p))
+    return m.value, p.value
+
+
+def kitc_tree_create():
+    h = C.c_void_p()
+    _call("kitc_tree_create", C.byref(h))
+    return h
+
+
+def kitc_build_tree(t, xyz_ptr, N, N0, stream_ptr):
+    return _call("kitc_build_tree", t, xyz_ptr, int(N), int(N0), stream_ptr)
+
+
+def kitc_tree_info(t):
+    nc, dep, nb, nd = C.c_int64(), C.c_int32(), C.c_int64(), C.c_int32()
+    _call("kitc_tree_info", t, C.byref(nc), C.byref(dep), C.byref(nb), C.byref(nd))
+    return nc.value, dep.value, nb.value, nd.value
+
+
+def kitc_modified_weights(t, kernel, n, w_ptr, cluster_begin, cluster_end, fhat_ptr, stream_ptr):
+    return _call("kitc_modified_weights", t, int(kernel), int(n), w_ptr, int(cluster_begin),
+                 int(cluster_end), fhat_ptr, stream_ptr)
+
+
+def kitc_eval(t, kernel, n, theta, N0, eps, self_mode, fhat_ptr, batch_begin, batch_end, out_ptr,
+              stats_ptr, stream_ptr):
+    return _call("kitc_eval", t, int(kernel), int(n), float(theta), int(N0), float(eps),
+                 int(self_mode), fhat_ptr, int(batch_begin), int(batch_end), out_ptr, stats_ptr,
+                 stream_ptr)
+
+
+def kitc_batch_targets(t, batch_end):
+    v = C.c_int64()
+    _call("kitc_batch_targets", t, int(batch_end), C.byref(v))
+    return v.value
+
+
+def kitc_direct(kernel, eps, self_mode, xt_ptr, Nt, xs_ptr, ws_ptr, Ns, out_ptr, stream_ptr):
+    return _call("kitc_direct", int(kernel), float(eps), int(self_mode), xt_ptr, int(Nt), xs_ptr,
+                 ws_ptr, int(Ns), out_ptr, stream_ptr)
+
+
+def kitc_rel_error(ref_ptr, approx_ptr, count, stream_ptr):
+    E = C.c_double()
+    _call("kitc_rel_error", ref_ptr, approx_ptr, int(count), C.byref(E), stream_ptr)
+    return E.value
+
+
+def kitc_launch_count():
+    return int(_lib.kitc_launch_count())
+
+
+def kitc_tree_free(t):
+    _lib.kitc_tree_free(t)
+
+
+# ---- torch convenience layer ---------------------------------------------------
+
+class Tree:
+    """A built KITC tree (library-owned device memory) over device particles X[N, 3]."""
+
+    def __init__(self, X, N0, stream=None):
+        self._h = kitc_tree_create()
+        self.build(X, N0, stream)
+
+    def build(self, X, N0, stream=None):
+        X = _dev_f64(X, 3)
+        self.N, self.N0 = X.shape[0], int(N0)
+        kitc_build_tree(self._h, _ptr(X), self.N, self.N0, _stream(stream))
+        self.nclusters, self.depth, self.nbatches, self.ndegenerate = kitc_tree_info(self._h)
+        return self
+
+    @property
+    def handle(self):
+        return self._h
+
+    def fhat_shape(self, kernel, n):
+        m, _ = kitc_kernel_dims(kernel)
+        return (self.nclusters, m, (n + 1) ** 3)
+
+    def modified_weights(self, kernel, n, W, cluster_range=None, fhat=None, stream=None):
+        m, _ = kitc_kernel_dims(kernel)
+        W = _dev_f64(W, m)
+        if fhat is None:
+            fhat = torch.empty(self.fhat_shape(kernel, n), dtype=torch.float64, device=W.device)
+        cb, ce = cluster_range if cluster_range is not None else (0, self.nclusters)
+        kitc_modified_weights(self._h, kernel, n, _ptr(W), cb, ce, _ptr(fhat), _stream(stream))
+        return fhat
+
+    def eval(self, kernel, n, theta, eps, fhat, out=None, batch_range=None, self_omit=True,
+             stats=False, stream=None):
+        _, p = kitc_kernel_dims(kernel)
+        dev = fhat.device
+        if out is None:
+            out = torch.zeros((self.N, p), dtype=torch.float64, device=dev)
+        st = torch.zeros((self.N, 5), dtype=torch.int64, device=dev) if stats else None
+        bb, be = batch_range if batch_range is not None else (0, self.nbatches)
+        kitc_eval(self._h, kernel, n, theta, self.N0, eps, SELF_OMIT if self_omit else SELF_INCLUDE,
+                  _ptr(fhat), bb, be, _ptr(out), _ptr(st), _stream(stream))
+        return (out, st) if stats else out
+
+    def batch_targets(self, batch_end):
+        return kitc_batch_targets(self._h, batch_end)
+
+    def export(self):
+        """Host copy of the structure (numpy) -- parity checks only."""
+        import numpy as np
+        k, N = self.nclusters, self.N
+        a = dict(perm=np.empty(N, np.int64), begin=np.empty(k, np.int64), end=np.empty(k, np.int64),
+                 level=np.empty(k, np.int32), parent=np.empty(k, np.int32),
+                 first_child=np.empty(k, np.int32), nchild=np.empty(k, np.int32),
+                 lo=np.empty((k, 3)), hi=np.empty((k, 3)))
+        vp = lambda x: C.c_void_p(x.ctypes.data)
+        _call("kitc_tree_export", self._h, *(vp(a[n]) for n in
+                                              ("perm", "begin", "end", "level", "parent", "first_child",
+                                               "nchild", "lo", "hi")))
+        return a
+
+    def export_ranges(self):
+        """Host copy of the cluster ranges only (begin, end)."""
+        import numpy as np
+        k = self.nclusters
+        b, e = np.empty(k, np.int64), np.empty(k, np.int64)
+        _call("kitc_tree_export", self._h, None, C.c_void_p(b.ctypes.data), C.c_void_p(e.ctypes.data),
+              None, None, None, None, None, None)
+        return {"begin": b, "end": e}
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            kitc_tree_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def direct(X, W, kernel, eps, self_omit=True, targets=None, out=None, stream=None):
+    """O(N^2) sum on the GPU. X[N,3], W[N,m] device fp64; targets default = X."""
+    m, p = kitc_kernel_dims(kernel)
+    X, W = _dev_f64(X, 3), _dev_f64(W, m)
+    T = X if targets is None else _dev_f64(targets, 3)
+    if out is None:
+        out = torch.empty((T.shape[0], p), dtype=torch.float64, device=X.device)
+    kitc_direct(kernel, eps, SELF_OMIT if self_omit else SELF_INCLUDE, _ptr(T), T.shape[0], _ptr(X),
+                _ptr(W), X.shape[0], _ptr(out), _stream(stream))
+    return out
+
+
+def rel_error(ref, approx, stream=None):
+    """E of Eq. error on the GPU (rows concatenated)."""
+    assert ref.shape == approx.shape and ref.is_contiguous() and approx.is_contiguous()
+    return kitc_rel_error(_ptr(ref), _ptr(approx), ref.numel(), _stream(stream))
+
+
+def treecode(X, W, kernel, n, theta, N0, eps, self_omit=True, stats=False, stream=None, tree=None):
+    """One-shot eval(kernel, n, theta, N0, eps): build tree, modified weights, evaluate.
+    Returns out[N, p] (original order) [, stats[N, 5]]."""
+    if isinstance(kernel, str):
+        kernel = KERNELS[kernel]
+    T = tree.build(X, N0, stream) if tree is not None else Tree(X, N0, stream)
+    fhat = T.modified_weights(kernel, n, W, stream=stream)
+    return T.eval(kernel, n, theta, eps, fhat, self_omit=self_omit, stats=stats, stream=stream)

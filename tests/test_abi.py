@@ -1,0 +1,76 @@
+"""C-ABI checks that need no GPU: libkitc.so builds for sm_100a, loads, and
+exports every symbol include/kitc.h declares; argument validation paths that
+return before any CUDA call."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1902_02250_b200 import build as B
+    B.build()
+    return C.CDLL(B.LIB)
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "kitc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(kitc_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("kitc_build_tree", "kitc_modified_weights", "kitc_eval", "kitc_direct"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_1902_02250_b200 import build as B
+    out = subprocess.run(["nm", "-D", "--defined-only", B.LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (kitc_\w+)", out))
+    for s in declared_symbols():
+        assert s in exported, s
+        assert hasattr(lib, s)
+
+
+def test_binding_names_match_header():
+    from paper_1902_02250_b200 import kitc
+    assert sorted(kitc.EXPORTS) == declared_symbols()
+
+
+def test_sm100a_code_present():
+    from paper_1902_02250_b200 import build as B
+    out = subprocess.run(["cuobjdump", "--list-elf", B.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_validation_without_gpu():
+    from paper_1902_02250_b200 import kitc
+    assert kitc.kitc_kernel_dims(kitc.STOKESLET) == (3, 3)
+    assert kitc.kitc_kernel_dims(kitc.ROTLET) == (3, 6)
+    assert kitc.kitc_kernel_dims(kitc.STOKESLET_ROTLET) == (6, 6)
+    with pytest.raises(kitc.KitcError) as e:
+        kitc.kitc_kernel_dims(5)
+    assert e.value.status == kitc.KITC_EINVAL
+    # direct: unknown kernel, SELF_OMIT with distinct target/source arrays, negative eps
+    fake = C.c_void_p(16)
+    with pytest.raises(kitc.KitcError):
+        kitc.kitc_direct(9, 0.01, kitc.SELF_INCLUDE, fake, 1, fake, fake, 1, fake, None)
+    with pytest.raises(kitc.KitcError):
+        kitc.kitc_direct(0, 0.01, kitc.SELF_OMIT, fake, 1, C.c_void_p(32), fake, 1, fake, None)
+    with pytest.raises(kitc.KitcError):
+        kitc.kitc_direct(0, -1.0, kitc.SELF_INCLUDE, fake, 1, fake, fake, 1, fake, None)
+    h = kitc.kitc_tree_create()
+    with pytest.raises(kitc.KitcError) as e:
+        kitc.kitc_build_tree(h, fake, 0, 10, None)           # N < 1
+    assert e.value.status == kitc.KITC_EINVAL
+    with pytest.raises(kitc.KitcError) as e:
+        kitc.kitc_tree_info(h)                                # not built
+    assert e.value.status == kitc.KITC_ESTATE
+    kitc.kitc_tree_free(h)

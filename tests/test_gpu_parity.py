@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Gates (BASELINE.json north_star): tree / permutation bit-exact; GPU direct vs
+oracle direct relative 2-norm <= 1e-12; GPU treecode vs oracle treecode at
+the same tree, n, theta <= 1e-10; per-target interaction counts equal
+(integers).  Parity metric = Eq. error with the oracle as the reference.
+"""
+import numpy as np
+import pytest
+
+import kitc_inputs as KI
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DIRECT_GATE = 1e-12
+TREE_GATE = 1e-10
+
+
+@pytest.fixture(scope="module")
+def K():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1902_02250_b200 import kitc
+    return kitc
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+# ---------------------------------------------------------------- direct sum
+@pytest.mark.parametrize("N,kern,eps,self_omit", [
+    (1000, 0, 0.01, True), (4099, 0, 0.01, True), (4099, 1, 0.01, True), (3001, 2, 0.05, True),
+    (1500, 0, 0.02, False), (1, 0, 1.0, False), (2, 1, 0.01, True), (257, 0, 0.0, True)])
+def test_direct_parity(K, N, kern, eps, self_omit):
+    m = O.DIMS[kern][0]
+    X, W = KI.particles(N, seed=N, m=m)
+    ref = O.direct(kern, eps, X, W, self_omit=self_omit)
+    got = host(K.direct(dev(X), dev(W), kern, eps, self_omit=self_omit))
+    if np.all(ref == 0):
+        assert np.all(got == 0)
+    else:
+        assert O.rel_error(ref, got) <= DIRECT_GATE
+
+
+# ---------------------------------------------------------------- tree
+def assert_same_tree(T, G):
+    assert T.nclusters == len(G["begin"])
+    assert np.array_equal(T.perm, G["perm"])
+    for k in ("begin", "end", "level", "parent", "first_child", "nchild"):
+        assert np.array_equal(getattr(T, k), G[k]), k
+    assert np.array_equal(T.lo, G["lo"]) and np.array_equal(T.hi, G["hi"])
+
+
+@pytest.mark.parametrize("N,N0,geom", [(1000, 100, "uniform"), (100_000, 500, "uniform"),
+                                       (50_000, 64, "sphere"), (20_000, 40, "slab"),
+                                       (5000, 1, "uniform"), (33, 100, "uniform")])
+def test_tree_bit_exact(K, N, N0, geom):
+    X, _ = KI.particles(N, geom, seed=7)
+    T = O.Tree(X, N0)
+    G = K.Tree(dev(X), N0)
+    assert (G.nclusters, G.depth, G.ndegenerate) == (T.nclusters, T.depth, T.ndegenerate)
+    assert_same_tree(T, G.export())
+
+
+def test_tree_degenerate_inputs(K):
+    cases = [np.zeros((10, 3)),
+             np.array([[0, 0, 0]] * 3 + [[1, 1, 1]] * 3, float),
+             np.array([[1.0, 0, 0], [np.nextafter(1.0, 2.0), 0, 0], [np.nextafter(1.0, 2.0), 0, 0]]),
+             np.array([[i, j, k] for k in (0, 1) for j in (0, 1) for i in (0, 1)], float)]
+    for X in cases:
+        T = O.Tree(X, 1)
+        G = K.Tree(dev(X), 1)
+        assert G.ndegenerate == T.ndegenerate
+        assert_same_tree(T, G.export())
+    with pytest.raises(K.KitcError) as e:
+        K.Tree(dev(np.array([[0.0, np.inf, 0.0], [1.0, 1.0, 1.0]])), 1)
+    assert e.value.status == K.KITC_EINVAL
+
+
+# ---------------------------------------------------------------- weights
+@pytest.mark.parametrize("N,N0,n,kern,geom", [(1000, 100, 4, 0, "uniform"), (20_000, 500, 8, 0, "uniform"),
+                                              (12_000, 50, 3, 2, "sphere"), (9000, 2000, 10, 1, "uniform")])
+def test_modified_weights_parity(K, N, N0, n, kern, geom):
+    m = O.DIMS[kern][0]
+    X, W = KI.particles(N, geom, seed=3, m=m)
+    T = O.Tree(X, N0)
+    ref = T.modified_weights(W, n)
+    G = K.Tree(dev(X), N0)
+    got = host(G.modified_weights(kern, n, dev(W)))
+    for c in range(T.nclusters):
+        nrm = np.linalg.norm(ref[c])
+        assert np.linalg.norm(got[c] - ref[c]) <= 1e-13 * max(nrm, 1e-300), c
+
+
+# ---------------------------------------------------------------- treecode
+def run_gpu(K, X, W, kern, n, theta, N0, eps, self_omit=True):
+    G = K.Tree(dev(X), N0)
+    fh = G.modified_weights(kern, n, dev(W))
+    out, st = G.eval(kern, n, theta, eps, fh, self_omit=self_omit, stats=True)
+    return host(out), host(st), G
+
+
+@pytest.mark.parametrize("N,N0,n,theta,kern,eps,geom", [
+    (1000, 100, 4, 0.7, 0, 0.01, "uniform"),      # C1
+    (8000, 200, 8, 0.7, 0, 0.01, "uniform"),
+    (8000, 200, 8, 0.7, 1, 0.01, "uniform"),      # rotlet
+    (6000, 100, 5, 0.6, 2, 0.05, "uniform"),      # Stokeslet + rotlet
+    (15000, 300, 6, 0.7, 0, 0.005, "sphere"),
+    (7000, 80, 3, 0.5, 0, 0.01, "slab"),
+    (3000, 30, 12, 0.7, 0, 0.01, "uniform"),      # generic (runtime-P) kernel
+    (600, 20, 2, 0.0, 0, 0.01, "uniform"),        # theta = 0 -> direct
+])
+def test_treecode_parity(K, N, N0, n, theta, kern, eps, geom):
+    m = O.DIMS[kern][0]
+    X, W = KI.particles(N, geom, seed=11, m=m)
+    T = O.Tree(X, N0)
+    ref, rst = T.treecode(kern, eps, n, theta, W, stats=True)
+    got, gst = run_gpu(K, X, W, kern, n, theta, N0, eps)
+    assert O.rel_error(ref, got) <= TREE_GATE
+    assert np.array_equal(rst.astype(np.int64), gst)
+
+
+def test_treecode_self_include(K):
+    X, W = KI.particles(4000, seed=2)
+    T = O.Tree(X, 150)
+    ref = T.treecode(0, 0.02, 6, 0.7, W, self_omit=False)
+    got, _, _ = run_gpu(K, X, W, 0, 6, 0.7, 150, 0.02, self_omit=False)
+    assert O.rel_error(ref, got) <= TREE_GATE
+
+
+def test_error_tracks_oracle_vs_n(K):
+    # E_gpu(n) tracks E_oracle(n) (north_star): same decisions, rounding-level diffs
+    X, W = KI.particles(5000, seed=0)
+    d_or = O.direct(0, 0.01, X, W)
+    d_gpu = host(K.direct(dev(X), dev(W), 0, 0.01))
+    T = O.Tree(X, 250)
+    for n in range(1, 11):
+        e_or = O.rel_error(d_or, T.treecode(0, 0.01, n, 0.7, W))
+        got, _, _ = run_gpu(K, X, W, 0, n, 0.7, 250, 0.01)
+        e_gpu = O.rel_error(d_gpu, got)
+        assert abs(e_gpu - e_or) <= 1e-9 * max(e_or, 1e-16) + 1e-12
+
+
+def test_split_ranges_bitwise_identical(K):
+    # the multi-GPU decomposition (cluster shards + batch shards) is result-invariant
+    X, W = KI.particles(30000, seed=5)
+    G = K.Tree(dev(X), 400)
+    full = G.modified_weights(0, 6, dev(W))
+    out_full = G.eval(0, 6, 0.7, 0.01, full)
+    parts = torch.zeros_like(full)
+    C = G.nclusters
+    for cb, ce in [(0, C // 3), (C // 3, C // 2), (C // 2, C)]:
+        G.modified_weights(0, 6, dev(W), cluster_range=(cb, ce), fhat=parts)
+    assert torch.equal(parts, full)
+    out = torch.zeros_like(out_full)
+    nb = G.nbatches
+    for bb, be in [(0, 17), (17, nb // 2), (nb // 2, nb)]:
+        G.eval(0, 6, 0.7, 0.01, parts, out=out, batch_range=(bb, be))
+    assert torch.equal(out, out_full)
+    # run-to-run determinism
+    G2 = K.Tree(dev(X), 400)
+    assert torch.equal(G2.eval(0, 6, 0.7, 0.01, G2.modified_weights(0, 6, dev(W))), out_full)
+
+
+def test_state_errors(K):
+    X, W = KI.particles(500, seed=1)
+    G = K.Tree(dev(X), 50)
+    fh = torch.zeros(G.fhat_shape(0, 4), dtype=torch.float64, device="cuda")
+    with pytest.raises(K.KitcError) as e:
+        G.eval(0, 4, 0.7, 0.01, fh)                          # weights not computed
+    assert e.value.status == K.KITC_ESTATE
+    G.modified_weights(0, 4, dev(W), fhat=fh)
+    with pytest.raises(K.KitcError):
+        G.eval(0, 5, 0.7, 0.01, fh)                          # n mismatch
+    with pytest.raises(K.KitcError):
+        K.kitc_eval(G.handle, 0, 4, 0.7, 51, 0.01, 0, K._ptr(fh), 0, 1, K._ptr(fh), None, K._stream())
+    with pytest.raises(K.KitcError):
+        G.eval(0, 4, 1.0, 0.01, fh)                          # theta >= 1
+
+
+# ---------------------------------------------------------------- full size (bench config C3)
+@pytest.mark.slow
+def test_C3_full_size_sampled(K):
+    c = KI.CONFIGS["C3"]
+    X, W = KI.config_particles("C3")
+    tg = KI.sample_targets(c["N"], 200, seed=3)
+    T = O.Tree(X, c["N0"])
+    F = T.modified_weights(W, c["n"])
+    ref, rst = T.treecode(0, c["eps"], c["n"], c["theta"], W, fhat=F, targets=tg, stats=True)
+    got, gst, G = run_gpu(K, X, W, 0, c["n"], c["theta"], c["N0"], c["eps"])
+    assert G.nclusters == T.nclusters and G.depth == T.depth
+    assert np.array_equal(G.export()["perm"], T.perm)
+    assert O.rel_error(ref, got[tg]) <= TREE_GATE
+    assert np.array_equal(rst.astype(np.int64), gst[tg])
+    # GPU fhat of the full tree vs the oracle's
+    fh = host(G.modified_weights(0, c["n"], dev(W)))
+    assert np.linalg.norm(fh - F) <= 1e-13 * np.linalg.norm(F)
+    # direct sum on a sample of targets
+    tg2 = tg[:40]
+    dref = O.direct(0, c["eps"], X, W, targets=tg2)
+    dgot = host(K.direct(dev(X), dev(W), 0, c["eps"]))
+    assert O.rel_error(dref, dgot[tg2]) <= DIRECT_GATE
+    E = O.rel_error(dgot, got)
+    assert 1e-9 < E < 1e-4
