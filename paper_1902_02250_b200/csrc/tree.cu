@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(kThreads) k_part_scatter(
             for (int k = 0; k < NW; ++k) s += wcnt[k][threadIdx.x];
             base[threadIdx.x] += s;
         }
+        __syncthreads();  // wcnt is cleared at the top of the next tile
     }
 }
 

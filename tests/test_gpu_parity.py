@@ -123,7 +123,7 @@ def test_treecode_parity(K, N, N0, n, theta, kern, eps, geom):
     X, W = KI.particles(N, geom, seed=11, m=m)
     T = O.Tree(X, N0)
     ref, rst = T.treecode(kern, eps, n, theta, W, stats=True)
-    got, gst = run_gpu(K, X, W, kern, n, theta, N0, eps)
+    got, gst, _ = run_gpu(K, X, W, kern, n, theta, N0, eps)
     assert O.rel_error(ref, got) <= TREE_GATE
     assert np.array_equal(rst.astype(np.int64), gst)
 
