@@ -1,7 +1,8 @@
 // eval.cu -- treecode evaluation (Algorithm 2 lines 7-17) on sm_100a.
 //
-// One warp = one batch of <= 32 consecutive sorted targets inside one leaf
-// (spatially coherent).  The warp walks the tree depth-first with an explicit
+// One warp = one batch of <= kBatch targets of one leaf, consecutive in the
+// leaf's Morton order (spatially compact); kGroup lanes cooperate on each
+// target (they split its proxies / sources and combine at the end).  The warp walks the tree depth-first with an explicit
 // shared-memory stack of (cluster, lane mask) entries, so every lane keeps the
 // paper's PER-TARGET semantics: a lane stops descending below a cluster it
 // accepted; lanes that reject a cluster descend into its children.  At each
@@ -30,6 +31,7 @@ struct EvalArgs {
     const double* y;
     const double* z;
     const int* perm;
+    const int* tord;
     const double* w;  // sorted weights, M planes of N
     const double4* cr;
     const int4* topo;
@@ -48,61 +50,63 @@ struct EvalArgs {
     KParams kp;
 };
 
+// Far field of one accepted cluster for the lanes of one target group: lane
+// group g (of kGroup) sums rows (k1, k2) = g, g + kGroup, ... of the (n+1)^2
+// rows, all k3 per row; partial sums are combined once per target at the end.
 template <int PT, int KER>
 __device__ __forceinline__ void far_field(double x, double y, double z, const double* __restrict__ g,
-                                          const double* __restrict__ F, double* acc, const KParams& kp, int Prt) {
+                                          const double* __restrict__ F, double* acc, const KParams& kp, int Prt,
+                                          int grp) {
     using K = Kern<KER>;
     constexpr int M = K::M;
     if constexpr (PT > 0) {
-        constexpr int P = PT, P3 = P * P * P;
+        constexpr int P = PT, P2 = P * P, P3 = P2 * P;
         double dz[P], ez[P];
 #pragma unroll
         for (int k3 = 0; k3 < P; ++k3) {
             dz[k3] = z - __ldg(g + 2 * P + k3);
             ez[k3] = fma(dz[k3], dz[k3], kp.e2);
         }
-        for (int k1 = 0; k1 < P; ++k1) {
+        for (int row = grp; row < P2; row += kGroup) {
+            const int k1 = row / P, k2 = row - k1 * P;
             const double dx = x - __ldg(g + k1);
-            const double dx2 = dx * dx;
-            for (int k2 = 0; k2 < P; ++k2) {
-                const double dy = y - __ldg(g + P + k2);
-                const double pxy = fma(dy, dy, dx2);
-                const double* Fk = F + (k1 * P + k2) * P;
+            const double dy = y - __ldg(g + P + k2);
+            const double pxy = fma(dy, dy, dx * dx);
+            const double* Fk = F + row * P;
 #pragma unroll
-                for (int k3 = 0; k3 < P; ++k3) {
-                    double f[M];
+            for (int k3 = 0; k3 < P; ++k3) {
+                double f[M];
 #pragma unroll
-                    for (int m = 0; m < M; ++m) f[m] = __ldg(Fk + m * P3 + k3);
-                    K::pair(dx, dy, dz[k3], pxy + ez[k3], f, acc, kp);
-                }
+                for (int m = 0; m < M; ++m) f[m] = __ldg(Fk + m * P3 + k3);
+                K::pair(dx, dy, dz[k3], pxy + ez[k3], f, acc, kp);
             }
         }
     } else {
-        const int P = Prt, P3 = P * P * P;
-        for (int k1 = 0; k1 < P; ++k1) {
+        const int P = Prt, P2 = P * P, P3 = P2 * P;
+        for (int row = grp; row < P2; row += kGroup) {
+            const int k1 = row / P, k2 = row - k1 * P;
             const double dx = x - __ldg(g + k1);
-            for (int k2 = 0; k2 < P; ++k2) {
-                const double dy = y - __ldg(g + P + k2);
-                const double pxy = fma(dy, dy, dx * dx);
-                const double* Fk = F + (k1 * P + k2) * P;
-                for (int k3 = 0; k3 < P; ++k3) {
-                    const double dz = z - __ldg(g + 2 * P + k3);
-                    double f[M];
+            const double dy = y - __ldg(g + P + k2);
+            const double pxy = fma(dy, dy, dx * dx);
+            const double* Fk = F + row * P;
+            for (int k3 = 0; k3 < P; ++k3) {
+                const double dz = z - __ldg(g + 2 * P + k3);
+                double f[M];
 #pragma unroll
-                    for (int m = 0; m < M; ++m) f[m] = __ldg(Fk + m * P3 + k3);
-                    K::pair(dx, dy, dz, pxy + fma(dz, dz, kp.e2), f, acc, kp);
-                }
+                for (int m = 0; m < M; ++m) f[m] = __ldg(Fk + m * P3 + k3);
+                K::pair(dx, dy, dz, pxy + fma(dz, dz, kp.e2), f, acc, kp);
             }
         }
     }
 }
 
+// Near field of one rejected leaf: lane group g sums sources b + g, b + g + kGroup, ...
 template <int KER>
-__device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e,
+__device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e, int grp,
                                            const EvalArgs& a, double* acc) {
     using K = Kern<KER>;
     constexpr int M = K::M;
-    for (int j = b; j < e; ++j) {
+    for (int j = b + grp; j < e; j += kGroup) {
         const double dx = x - __ldg(a.x + j), dy = y - __ldg(a.y + j), dz = z - __ldg(a.z + j);
         double f[M];
 #pragma unroll
@@ -112,18 +116,21 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
     }
 }
 
+// Lane l works for target l / kGroup of the batch, as member l % kGroup of its
+// group; the kGroup lanes of a target share every MAC decision.
 template <int PT, int KER>
 __global__ void __launch_bounds__(kWarps * 32) k_eval(const EvalArgs a) {
     using K = Kern<KER>;
     constexpr int M = K::M, NP = K::P;
     extern __shared__ int2 smem_stack[];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int grp = lane % kGroup, ti = lane / kGroup;
     int2* stk = smem_stack + wl * a.stack_cap;
     const long long b = a.bb + (long long)blockIdx.x * kWarps + wl;
     if (b >= a.be) return;  // whole warp
-    const int t0 = a.bstart[b], tc = a.bcount[b];
-    const bool valid = lane < tc;
-    const int t = t0 + (valid ? lane : 0);
+    const int p0 = a.bstart[b], tc = a.bcount[b];
+    const bool valid = ti < tc;
+    const int t = a.tord[p0 + (valid ? ti : 0)];
     const double x = a.x[t], y = a.y[t], z = a.z[t];
     const int P = PT > 0 ? PT : a.P;
     const int P3 = P * P * P;
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_eval(const EvalArgs a) {
         const unsigned rm = mask & ~am;
         const int4 tp = a.topo[c];
         if (am && ok) {
-            far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * M * P3, acc, a.kp, P);
+            far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * M * P3, acc, a.kp, P, grp);
             if (a.stats) {
                 st[0] += 1;
                 st[1] += (unsigned long long)P3;
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_eval(const EvalArgs a) {
         if (rm) {
             if (tp.w == 0) {
                 if (in && !ok) {
-                    near_field<KER>(x, y, z, t, tp.x, tp.y, a, acc);
+                    near_field<KER>(x, y, z, t, tp.x, tp.y, grp, a, acc);
                     if (a.stats) {
                         const int self = (a.self_omit && t >= tp.x && t < tp.y) ? 1 : 0;
                         st[2] += 1;
@@ -179,7 +186,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_eval(const EvalArgs a) {
             }
         }
     }
-    if (!valid) return;
+    // combine the kGroup partial sums of each target (fixed order -> deterministic)
+#pragma unroll
+    for (int c = 0; c < NP; ++c)
+#pragma unroll
+        for (int o = 1; o < kGroup; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    if (!valid || grp != 0) return;
     const int o = a.perm[t];
 #pragma unroll
     for (int c = 0; c < NP; ++c) a.out[(size_t)o * NP + c] = acc[c] * K::scale(c);
@@ -230,6 +242,7 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     a.y = t->y.as<double>();
     a.z = t->z.as<double>();
     a.perm = t->perm.as<int>();
+    a.tord = t->tord.as<int>();
     a.w = t->w.as<double>();
     a.cr = t->cr.as<double4>();
     a.topo = t->topo.as<int4>();

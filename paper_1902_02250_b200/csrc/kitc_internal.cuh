@@ -12,7 +12,11 @@
 namespace kitc {
 
 constexpr int kMaxDegree = 16;        // n in [1, 16]
-constexpr int kBatch = 32;            // targets per warp batch
+#ifndef KITC_GROUP
+#define KITC_GROUP 4
+#endif
+constexpr int kGroup = KITC_GROUP;    // lanes cooperating on one target in k_eval
+constexpr int kBatch = 32 / kGroup;   // targets per warp batch
 constexpr double kPi = 3.14159265358979323846;
 
 extern std::atomic<unsigned long long> g_launches;  // kernels launched by the library
@@ -73,7 +77,9 @@ struct kitc_tree {
     kitc::DevBuf cr;     // double4[C]    centre xyz, r^2
     kitc::DevBuf topo;   // int4[C]       begin, end, first_child, nchild
     kitc::DevBuf grid;   // double[C][3][n+1]
-    kitc::DevBuf bstart; // int32[nbatches] first target of the batch (sorted index)
+    kitc::DevBuf tord;   // int32[N] targets in Morton order inside each leaf (batching only)
+    kitc::DevBuf leaves; // int4[nleaves] begin, end, cluster id
+    kitc::DevBuf bstart; // int32[nbatches] first position (in tord) of the batch
     kitc::DevBuf bcount; // int32[nbatches]
 
     // host mirrors of the topology

@@ -227,6 +227,69 @@ __global__ void __launch_bounds__(kThreads) k_copy_back(const Item* __restrict__
     }
 }
 
+// Targets of each leaf in Morton order of their position inside the leaf box,
+// so that a warp batch (kBatch consecutive entries) is spatially compact and
+// its lanes take the same MAC decisions more often.  Batching only: every
+// target's traversal and sums are independent of it.  Leaves larger than
+// kSortMax (degenerate ones) keep their sorted order.
+constexpr int kSortMax = 2048;
+
+__device__ __forceinline__ unsigned int spread3(unsigned int v) {  // 10 bits -> every 3rd bit
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_leaf_order(const int4* __restrict__ leaves, const double* __restrict__ box,
+                                                    const double* __restrict__ x, const double* __restrict__ y,
+                                                    const double* __restrict__ z, int* __restrict__ tord) {
+    __shared__ unsigned long long key[kSortMax];
+    const int4 lf = leaves[blockIdx.x];
+    const int b = lf.x, n = lf.y - lf.x, c = lf.z;
+    if (n > kSortMax) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) tord[b + i] = b + i;
+        return;
+    }
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    double lo[3], sc[3];
+    for (int l = 0; l < 3; ++l) {
+        lo[l] = box[(size_t)c * 6 + l];
+        const double w = box[(size_t)c * 6 + 3 + l] - lo[l];
+        sc[l] = w > 0.0 ? 1023.999 / w : 0.0;
+    }
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        unsigned long long k = ~0ull;
+        if (i < n) {
+            const unsigned qx = (unsigned)fmin(fmax((x[b + i] - lo[0]) * sc[0], 0.0), 1023.0);
+            const unsigned qy = (unsigned)fmin(fmax((y[b + i] - lo[1]) * sc[1], 0.0), 1023.0);
+            const unsigned qz = (unsigned)fmin(fmax((z[b + i] - lo[2]) * sc[2], 0.0), 1023.0);
+            const unsigned m = spread3(qx) | (spread3(qy) << 1) | (spread3(qz) << 2);
+            k = ((unsigned long long)m << 32) | (unsigned)i;
+        }
+        key[i] = k;
+    }
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long a = key[i], bb = key[ixj];
+                    if ((a > bb) == ((i & k) == 0)) {
+                        key[i] = bb;
+                        key[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) tord[b + i] = b + (int)(key[i] & 0xffffffffu);
+}
+
 template <class T>
 static size_t pad16(size_t n) {
     return (n * sizeof(T) + 15) / 16 * 16;
@@ -426,19 +489,27 @@ kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N64, int32_t N0,
         }
     }
     const int nb = (int)t->h_bstart.size();
+    const int nlv = (int)leaves.size();
     t->nbatches = nb;
-    const size_t q1 = pad16<int4>(C), q2 = q1 + pad16<int>(nb), q3 = q2 + pad16<int>(nb);
-    KITC_TRY(t->h_stage.ensure(q3));
+    const size_t q1 = pad16<int4>(C), q2 = q1 + pad16<int>(nb), q3 = q2 + pad16<int>(nb), q4 = q3 + pad16<int4>(nlv);
+    KITC_TRY(t->h_stage.ensure(q4));
     int4* ht = t->h_stage.as<int4>();
     for (int c = 0; c < C; ++c) ht[c] = make_int4(hb[c], he[c], hf[c], hn[c]);
     std::copy(t->h_bstart.begin(), t->h_bstart.end(), reinterpret_cast<int*>(t->h_stage.as<char>() + q1));
     std::copy(t->h_bcount.begin(), t->h_bcount.end(), reinterpret_cast<int*>(t->h_stage.as<char>() + q2));
+    int4* hlv = reinterpret_cast<int4*>(t->h_stage.as<char>() + q3);
+    for (int i = 0; i < nlv; ++i) hlv[i] = make_int4(hb[leaves[i].second], he[leaves[i].second], leaves[i].second, 0);
     KITC_TRY(t->topo.ensure(q1, s));
     KITC_TRY(t->bstart.ensure(q2 - q1, s));
     KITC_TRY(t->bcount.ensure(q3 - q2, s));
+    KITC_TRY(t->leaves.ensure(q4 - q3, s));
+    KITC_TRY(t->tord.ensure((size_t)N * sizeof(int), s));
     KITC_CUDA(cudaMemcpyAsync(t->topo.p, t->h_stage.p, (size_t)C * sizeof(int4), cudaMemcpyHostToDevice, s));
     KITC_CUDA(cudaMemcpyAsync(t->bstart.p, t->h_stage.as<char>() + q1, (size_t)nb * sizeof(int), cudaMemcpyHostToDevice, s));
     KITC_CUDA(cudaMemcpyAsync(t->bcount.p, t->h_stage.as<char>() + q2, (size_t)nb * sizeof(int), cudaMemcpyHostToDevice, s));
+    KITC_CUDA(cudaMemcpyAsync(t->leaves.p, hlv, (size_t)nlv * sizeof(int4), cudaMemcpyHostToDevice, s));
+    k_leaf_order<<<nlv, 256, 0, s>>>(t->leaves.as<int4>(), t->box.as<double>(), x, y, z, t->tord.as<int>()); note_launch();
+    KITC_CUDA(cudaGetLastError());
     KITC_CUDA(cudaStreamSynchronize(s));
     t->built = true;
     return KITC_OK;

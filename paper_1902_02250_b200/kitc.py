@@ -19,7 +19,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkitc.so")
+LIB_PATH = os.environ.get("KITC_LIB") or os.path.join(_HERE, "libkitc.so")  # override: tuning builds only
 
 KITC_OK, KITC_EINVAL, KITC_ENOMEM, KITC_ECUDA, KITC_ESTATE = 0, -1, -2, -3, -4
 STOKESLET, ROTLET, STOKESLET_ROTLET = 0, 1, 2
