@@ -24,7 +24,13 @@ namespace kitc {
 
 namespace {
 
-constexpr int kWarps = 4;  // warps (batches) per CTA
+#ifndef KITC_EVAL_WARPS
+#define KITC_EVAL_WARPS 4
+#endif
+#ifndef KITC_EVAL_MINB
+#define KITC_EVAL_MINB 6
+#endif
+constexpr int kWarps = KITC_EVAL_WARPS;  // warps (batches) per CTA
 
 struct EvalArgs {
     const double* x;
@@ -105,21 +111,47 @@ template <int KER>
 __device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e, int grp,
                                            const EvalArgs& a, double* acc) {
     using K = Kern<KER>;
-    constexpr int M = K::M;
-    for (int j = b + grp; j < e; j += kGroup) {
+    constexpr int M = K::M, U = 4;
+    // The self pair (j == t under SELF_OMIT) is evaluated with f = 0 and s = 1:
+    // its contribution is exactly zero, so the loop stays branch-free.
+    const int self = a.self_omit ? t : -1;
+    int j = b + grp;
+    for (; j + (U - 1) * kGroup < e; j += U * kGroup) {
+        double sx[U], sy[U], sz[U], f[U][M];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int jj = j + u * kGroup;
+            sx[u] = __ldg(a.x + jj);
+            sy[u] = __ldg(a.y + jj);
+            sz[u] = __ldg(a.z + jj);
+#pragma unroll
+            for (int m = 0; m < M; ++m) f[u][m] = __ldg(a.w + (size_t)m * a.N + jj);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool me = (j + u * kGroup) == self;
+            const double dx = x - sx[u], dy = y - sy[u], dz = z - sz[u];
+#pragma unroll
+            for (int m = 0; m < M; ++m) f[u][m] = me ? 0.0 : f[u][m];
+            const double s = me ? 1.0 : fma(dx, dx, fma(dy, dy, fma(dz, dz, a.kp.e2)));
+            K::pair(dx, dy, dz, s, f[u], acc, a.kp);
+        }
+    }
+    for (; j < e; j += kGroup) {
+        const bool me = j == self;
         const double dx = x - __ldg(a.x + j), dy = y - __ldg(a.y + j), dz = z - __ldg(a.z + j);
         double f[M];
 #pragma unroll
-        for (int m = 0; m < M; ++m) f[m] = __ldg(a.w + (size_t)m * a.N + j);
-        const double s = fma(dx, dx, fma(dy, dy, fma(dz, dz, a.kp.e2)));
-        if (j != t || !a.self_omit) K::pair(dx, dy, dz, s, f, acc, a.kp);
+        for (int m = 0; m < M; ++m) f[m] = me ? 0.0 : __ldg(a.w + (size_t)m * a.N + j);
+        const double s = me ? 1.0 : fma(dx, dx, fma(dy, dy, fma(dz, dz, a.kp.e2)));
+        K::pair(dx, dy, dz, s, f, acc, a.kp);
     }
 }
 
 // Lane l works for target l / kGroup of the batch, as member l % kGroup of its
 // group; the kGroup lanes of a target share every MAC decision.
 template <int PT, int KER>
-__global__ void __launch_bounds__(kWarps * 32) k_eval(const EvalArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, KITC_EVAL_MINB) k_eval(const EvalArgs a) {
     using K = Kern<KER>;
     constexpr int M = K::M, NP = K::P;
     extern __shared__ int2 smem_stack[];

@@ -13,7 +13,7 @@ namespace kitc {
 
 constexpr int kMaxDegree = 16;        // n in [1, 16]
 #ifndef KITC_GROUP
-#define KITC_GROUP 4
+#define KITC_GROUP 8
 #endif
 constexpr int kGroup = KITC_GROUP;    // lanes cooperating on one target in k_eval
 constexpr int kBatch = 32 / kGroup;   // targets per warp batch
