@@ -85,8 +85,8 @@ kitc_status kitc_build_tree(kitc_tree* t, const double* xyz_dev, int64_t N, int3
 
 /* Sizes of the built tree.  Any output pointer may be NULL.
  *  n_clusters: number of clusters C (BFS order: by level, then by range start);
- *  depth: deepest level (root = 0); n_batches: number of 32-target batches
- *  (batches never straddle a leaf; ordered by target position);
+ *  depth: deepest level (root = 0); n_batches: number of warp batches of
+ *  <= 4 targets (never straddling a leaf; ordered by leaf, Morton order inside);
  *  n_degenerate: leaves with count > N0 (coincident points). */
 kitc_status kitc_tree_info(const kitc_tree* t, int64_t* n_clusters, int32_t* depth,
                            int64_t* n_batches, int32_t* n_degenerate);
@@ -109,8 +109,9 @@ kitc_status kitc_tree_export(const kitc_tree* t, int64_t* perm_host, int64_t* be
  * exactly), simple weights (-1)^k delta_k, and the coincidence flag
  * |y - s_k| <= DBL_MIN -> L = e_k (last k wins).
  *  w_dev: device, double[N][m] in ORIGINAL order (m from kitc_kernel_dims).
- *  fhat_dev: device, double[C][m][(n+1)^3] (k3 fastest); only the requested
- *  clusters' slices are written.  Also gathers w into the tree's sorted
+ *  fhat_dev: device, double[C][(n+1)^3 m] in the order [c][k3][comp][k1 (n+1) + k2]
+ *  (per cluster: n+1 planes of m components, each holding the (n+1)^2 rows
+ *  (k1, k2) contiguously); only the requested clusters' slices are written.  Also gathers w into the tree's sorted
  *  layout and computes every cluster's grid (both used by kitc_eval).
  *  0 <= cluster_begin <= cluster_end <= C.  ESTATE if no tree is built. */
 kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const double* w_dev,
@@ -126,7 +127,7 @@ kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const
  * rejected internal -> children.
  *  n, kernel: must match the last kitc_modified_weights call; N0 must equal
  *  the tree's N0; 0 <= theta < 1; eps >= 0 (eps = 0 requires SELF_OMIT).
- *  fhat_dev: the FULL double[C][m][(n+1)^3] (every cluster a target may accept).
+ *  fhat_dev: the FULL double[C][(n+1)^3 m] of kitc_modified_weights (every cluster).
  *  out_dev: device double[N][p], original order; only the targets of the given
  *  batches are written.
  *  stats_dev: optional (NULL = off) device uint64[N][5], original order:

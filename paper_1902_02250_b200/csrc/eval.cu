@@ -63,46 +63,57 @@ template <int PT, int KER>
 __device__ __forceinline__ void far_field(double x, double y, double z, const double* __restrict__ g,
                                           const double* __restrict__ F, double* acc, const KParams& kp, int Prt,
                                           int grp) {
+    // F layout: F[k3][m][row], row = k1 (n+1) + k2 (weights.cu).  Group g takes
+    // rows g, g + kGroup, ...; the rows left after the last full round are
+    // split pair by pair over the groups (balance).
     using K = Kern<KER>;
     constexpr int M = K::M;
+    const int P = PT > 0 ? PT : Prt, P2 = P * P;
+    const int full = (P2 / kGroup) * kGroup;
     if constexpr (PT > 0) {
-        constexpr int P = PT, P2 = P * P, P3 = P2 * P;
-        double dz[P], ez[P];
+        double dz[PT], ez[PT];
 #pragma unroll
-        for (int k3 = 0; k3 < P; ++k3) {
-            dz[k3] = z - __ldg(g + 2 * P + k3);
+        for (int k3 = 0; k3 < PT; ++k3) {
+            dz[k3] = z - __ldg(g + 2 * PT + k3);
             ez[k3] = fma(dz[k3], dz[k3], kp.e2);
         }
-        for (int row = grp; row < P2; row += kGroup) {
-            const int k1 = row / P, k2 = row - k1 * P;
+        for (int row = grp; row < full; row += kGroup) {
+            const int k1 = row / PT, k2 = row - k1 * PT;
             const double dx = x - __ldg(g + k1);
-            const double dy = y - __ldg(g + P + k2);
+            const double dy = y - __ldg(g + PT + k2);
             const double pxy = fma(dy, dy, dx * dx);
-            const double* Fk = F + row * P;
 #pragma unroll
-            for (int k3 = 0; k3 < P; ++k3) {
+            for (int k3 = 0; k3 < PT; ++k3) {
                 double f[M];
 #pragma unroll
-                for (int m = 0; m < M; ++m) f[m] = __ldg(Fk + m * P3 + k3);
+                for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
                 K::pair(dx, dy, dz[k3], pxy + ez[k3], f, acc, kp);
             }
         }
     } else {
-        const int P = Prt, P2 = P * P, P3 = P2 * P;
-        for (int row = grp; row < P2; row += kGroup) {
+        for (int row = grp; row < full; row += kGroup) {
             const int k1 = row / P, k2 = row - k1 * P;
             const double dx = x - __ldg(g + k1);
             const double dy = y - __ldg(g + P + k2);
             const double pxy = fma(dy, dy, dx * dx);
-            const double* Fk = F + row * P;
             for (int k3 = 0; k3 < P; ++k3) {
                 const double dz = z - __ldg(g + 2 * P + k3);
                 double f[M];
 #pragma unroll
-                for (int m = 0; m < M; ++m) f[m] = __ldg(Fk + m * P3 + k3);
+                for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
                 K::pair(dx, dy, dz, pxy + fma(dz, dz, kp.e2), f, acc, kp);
             }
         }
+    }
+    const int rem = (P2 - full) * P;  // pairs of the leftover rows
+    for (int q = grp; q < rem; q += kGroup) {
+        const int row = full + q / P, k3 = q - (q / P) * P;
+        const int k1 = row / P, k2 = row - k1 * P;
+        const double dx = x - __ldg(g + k1), dy = y - __ldg(g + P + k2), dz = z - __ldg(g + 2 * P + k3);
+        double f[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
+        K::pair(dx, dy, dz, fma(dy, dy, dx * dx) + fma(dz, dz, kp.e2), f, acc, kp);
     }
 }
 

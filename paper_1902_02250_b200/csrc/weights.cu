@@ -8,6 +8,9 @@
 // last k wins) and stages them with the weights in shared memory; phase 2 has
 // thread (k2, k3) accumulate fhat[m][k1][k2][k3] += Lx[k1] (Ly[k2] Lz[k3] f_m)
 // in registers for all k1 and m (the tensor-product loop of lines 20-22).
+// Layout (include/kitc.h): fhat[c][k3][m][k1 (n+1) + k2] -- the (n+1)^2 rows
+// (k1, k2) of one (k3, m) plane are contiguous, so the kGroup lane groups of
+// k_eval, which take consecutive rows, read one contiguous segment per load.
 // Chunks of one cluster write partials that a second kernel sums in chunk
 // order (deterministic).  Reading A15: L per axis instead of
 // (a1 a2 a3 / denom) -- rounding-only difference.
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__((P * P + 31) / 32 * 32) k_weights(
 #pragma unroll
     for (int m = 0; m < M; ++m)
 #pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) dst[m * P3 + k1 * P2 + tid] = acc[m][k1];
+        for (int k1 = 0; k1 < P; ++k1) dst[(k3 * M + m) * P2 + k1 * P + k2] = acc[m][k1];
 }
 
 struct RItem {

@@ -35,6 +35,14 @@ def host(t):
     return t.cpu().numpy()
 
 
+def fhat_to_oracle(F, n):
+    """GPU fhat [C][k3][m][k1 (n+1) + k2] -> oracle [C][m][(k1 (n+1) + k2) (n+1) + k3]."""
+    P = n + 1
+    C = F.shape[0]
+    m = F.size // (C * P ** 3)
+    return np.ascontiguousarray(F.reshape(C, P, m, P, P).transpose(0, 2, 3, 4, 1)).reshape(C, m, P ** 3)
+
+
 # ---------------------------------------------------------------- direct sum
 @pytest.mark.parametrize("N,kern,eps,self_omit", [
     (1000, 0, 0.01, True), (4099, 0, 0.01, True), (4099, 1, 0.01, True), (3001, 2, 0.05, True),
@@ -94,7 +102,7 @@ def test_modified_weights_parity(K, N, N0, n, kern, geom):
     T = O.Tree(X, N0)
     ref = T.modified_weights(W, n)
     G = K.Tree(dev(X), N0)
-    got = host(G.modified_weights(kern, n, dev(W)))
+    got = fhat_to_oracle(host(G.modified_weights(kern, n, dev(W))), n)
     for c in range(T.nclusters):
         nrm = np.linalg.norm(ref[c])
         assert np.linalg.norm(got[c] - ref[c]) <= 1e-13 * max(nrm, 1e-300), c
@@ -201,7 +209,7 @@ def test_C3_full_size_sampled(K):
     assert O.rel_error(ref, got[tg]) <= TREE_GATE
     assert np.array_equal(rst.astype(np.int64), gst[tg])
     # GPU fhat of the full tree vs the oracle's
-    fh = host(G.modified_weights(0, c["n"], dev(W)))
+    fh = fhat_to_oracle(host(G.modified_weights(0, c["n"], dev(W))), c["n"])
     assert np.linalg.norm(fh - F) <= 1e-13 * np.linalg.norm(F)
     # direct sum on a sample of targets
     tg2 = tg[:40]
