@@ -58,14 +58,14 @@ struct EvalArgs {
 
 // Far field of one accepted cluster for the lanes of one target group: lane
 // group g (of kGroup) sums rows (k1, k2) = g, g + kGroup, ... of the (n+1)^2
-// rows, all k3 per row; partial sums are combined once per target at the end.
+// rows, all k3 per row (dx, dy, dx^2 + dy^2 per row and dz, dz^2 + eps^2 per
+// plane are reused; Kern::pair_row folds the terms linear in d along the row);
+// the rows left after the last full round are split pair by pair over the
+// groups.  F layout: F[k3][m][row], row = k1 (n+1) + k2 (weights.cu).
 template <int PT, int KER>
 __device__ __forceinline__ void far_field(double x, double y, double z, const double* __restrict__ g,
                                           const double* __restrict__ F, double* acc, const KParams& kp, int Prt,
                                           int grp) {
-    // F layout: F[k3][m][row], row = k1 (n+1) + k2 (weights.cu).  Group g takes
-    // rows g, g + kGroup, ...; the rows left after the last full round are
-    // split pair by pair over the groups (balance).
     using K = Kern<KER>;
     constexpr int M = K::M;
     const int P = PT > 0 ? PT : Prt, P2 = P * P;
@@ -82,13 +82,21 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
             const double dx = x - __ldg(g + k1);
             const double dy = y - __ldg(g + PT + k2);
             const double pxy = fma(dy, dy, dx * dx);
+            typename K::Row r;
 #pragma unroll
             for (int k3 = 0; k3 < PT; ++k3) {
                 double f[M];
 #pragma unroll
-                for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
-                K::pair(dx, dy, dz[k3], pxy + ez[k3], f, acc, kp);
+                for (int m = 0; m < M; ++m) {
+#ifdef KITC_EXPT_NOLOAD  // timing experiment only: one load per (row, m)
+                    f[m] = __ldg(F + m * P2 + row) + k3;
+#else
+                    f[m] = __ldg(F + (k3 * M + m) * P2 + row);
+#endif
+                }
+                K::pair_row(dx, dy, dz[k3], rsqrt_fast(pxy + ez[k3]), f, acc, r, kp);
             }
+            K::row_end(dx, dy, r, acc);
         }
     } else {
         for (int row = grp; row < full; row += kGroup) {
@@ -96,13 +104,15 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
             const double dx = x - __ldg(g + k1);
             const double dy = y - __ldg(g + P + k2);
             const double pxy = fma(dy, dy, dx * dx);
+            typename K::Row r;
             for (int k3 = 0; k3 < P; ++k3) {
                 const double dz = z - __ldg(g + 2 * P + k3);
                 double f[M];
 #pragma unroll
                 for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
-                K::pair(dx, dy, dz, pxy + fma(dz, dz, kp.e2), f, acc, kp);
+                K::pair_row(dx, dy, dz, rsqrt_fast(pxy + fma(dz, dz, kp.e2)), f, acc, r, kp);
             }
+            K::row_end(dx, dy, r, acc);
         }
     }
     const int rem = (P2 - full) * P;  // pairs of the leftover rows
@@ -118,6 +128,7 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
 }
 
 // Near field of one rejected leaf: lane group g sums sources b + g, b + g + kGroup, ...
+// (unrolled x4 with the loads hoisted).
 template <int KER>
 __device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e, int grp,
                                            const EvalArgs& a, double* acc) {
