@@ -77,10 +77,20 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
             dz[k3] = z - __ldg(g + 2 * PT + k3);
             ez[k3] = fma(dz[k3], dz[k3], kp.e2);
         }
+        // the next row's grid coordinates are loaded one row ahead
+        double gx = 0.0, gy = 0.0;
+        if (grp < full) {
+            gx = __ldg(g + grp / PT);
+            gy = __ldg(g + PT + grp % PT);
+        }
         for (int row = grp; row < full; row += kGroup) {
-            const int k1 = row / PT, k2 = row - k1 * PT;
-            const double dx = x - __ldg(g + k1);
-            const double dy = y - __ldg(g + PT + k2);
+            const double dx = x - gx;
+            const double dy = y - gy;
+            const int nrow = row + kGroup;
+            if (nrow < full) {
+                gx = __ldg(g + nrow / PT);
+                gy = __ldg(g + PT + nrow % PT);
+            }
             const double pxy = fma(dy, dy, dx * dx);
             typename K::Row r;
 #pragma unroll
