@@ -115,7 +115,7 @@ def oracle_sample(cfg, X, W, S_targets, weight_frac=0.1, seed=1, fhat=None):
     F = np.zeros((T.nclusters, 3, (cfg["n"] + 1) ** 3)) if fhat is None else fhat.copy()
     t0 = time.perf_counter()
     T.modified_weights(W, cfg["n"], cluster_range=(cb, T.nclusters), out=F)
-    t_w = (time.perf_counter() - t0) * tot / acc
+    t_w = (time.perf_counter() - t0) * tot / acc if acc > 0 else 0.0
     if fhat is None:
         F = T.modified_weights(W, cfg["n"], cluster_range=(1, T.nclusters), out=F)
     tg = KI.sample_targets(N, S_targets, seed=seed)
