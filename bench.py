@@ -29,6 +29,15 @@ sys.path.insert(0, ROOT)
 import kitc_inputs as KI  # noqa: E402
 
 METRIC = "KITC Stokeslet targets/s, N=1e6 n=8 θ=0.7, 1/2/4/8 B200; % of FP64 peak"
+KNAME = {0: "Stokeslet", 1: "rotlet", 2: "Stokeslet+rotlet"}
+
+
+def metric_for(config):
+    """BASELINE.json's metric for the headline config C3; the same wording for the others."""
+    if config == "C3":
+        return METRIC
+    c = KI.CONFIGS[config]
+    return f"KITC {KNAME[c['kernel']]} targets/s, N={c['N']:.0e} n={c['n']} θ={c['theta']} ({config}); % of FP64 peak"
 UNIT = "targets/s"
 FLOPS_PER_PAIR = {0: 32, 1: 59, 2: 91}   # algorithmic flops per pair (DESIGN.md "Roofline")
 PEAK_SMS, PEAK_FMA_PER_CLK = 148, 64     # B200: 148 SMs x 64 FP64 FMA/clk/SM
@@ -146,7 +155,7 @@ def run_reference(args, cfg, rank):
     val = cfg["N"] / tstep
     sample = (f"per step: full oracle tree build; Algorithm 1 on the last clusters holding >=10% of "
               f"sum N_C (time x sum N_C ratio); Algorithm 2 on {S} random targets (time x N/{S})")
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": metric_for(args.config), "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tstep * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (kitc_inputs, seed 0)",
@@ -309,7 +318,7 @@ def run_kitc(args, cfg, rank, world, local_rank):
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": "full oracle tree; Algorithm 1 on clusters holding >=10% of sum N_C "
                          "(x sum N_C ratio); Algorithm 2 on 1500 random targets (x N/1500)", **det}
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    line = {"metric": metric_for(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (kitc_inputs: uniform [-1,1]^3, seed 0)",
