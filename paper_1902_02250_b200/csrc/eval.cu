@@ -66,17 +66,14 @@ template <int PT, int KER>
 __device__ __forceinline__ void far_field(double x, double y, double z, const double* __restrict__ g,
                                           const double* __restrict__ F, double* acc, const KParams& kp, int Prt,
                                           int grp) {
-    using K = Kern<KER>;
+    using K = EvalKern<KER>;
     constexpr int M = K::M;
     const int P = PT > 0 ? PT : Prt, P2 = P * P;
     const int full = (P2 / kGroup) * kGroup;
     if constexpr (PT > 0) {
-        double dz[PT], ez[PT];
+        double dz[PT];
 #pragma unroll
-        for (int k3 = 0; k3 < PT; ++k3) {
-            dz[k3] = z - __ldg(g + 2 * PT + k3);
-            ez[k3] = fma(dz[k3], dz[k3], kp.e2);
-        }
+        for (int k3 = 0; k3 < PT; ++k3) dz[k3] = z - __ldg(g + 2 * PT + k3);
         // the next row's grid coordinates are loaded one row ahead
         double gx = 0.0, gy = 0.0;
         if (grp < full) {
@@ -91,20 +88,14 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
                 gx = __ldg(g + nrow / PT);
                 gy = __ldg(g + PT + nrow % PT);
             }
-            const double pxy = fma(dy, dy, dx * dx);
+            const double pxye = fma(dy, dy, dx * dx) + kp.e2;
             typename K::Row r;
 #pragma unroll
             for (int k3 = 0; k3 < PT; ++k3) {
                 double f[M];
 #pragma unroll
-                for (int m = 0; m < M; ++m) {
-#ifdef KITC_EXPT_NOLOAD  // timing experiment only: one load per (row, m)
-                    f[m] = __ldg(F + m * P2 + row) + k3;
-#else
-                    f[m] = __ldg(F + (k3 * M + m) * P2 + row);
-#endif
-                }
-                K::pair_row(dx, dy, dz[k3], rsqrt_fast(pxy + ez[k3]), f, acc, r, kp);
+                for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
+                K::pair_row(dx, dy, dz[k3], fma(dz[k3], dz[k3], pxye), f, acc, r, kp);
             }
             K::row_end(dx, dy, r, acc);
         }
@@ -113,14 +104,14 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
             const int k1 = row / P, k2 = row - k1 * P;
             const double dx = x - __ldg(g + k1);
             const double dy = y - __ldg(g + P + k2);
-            const double pxy = fma(dy, dy, dx * dx);
+            const double pxye = fma(dy, dy, dx * dx) + kp.e2;
             typename K::Row r;
             for (int k3 = 0; k3 < P; ++k3) {
                 const double dz = z - __ldg(g + 2 * P + k3);
                 double f[M];
 #pragma unroll
                 for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
-                K::pair_row(dx, dy, dz, rsqrt_fast(pxy + fma(dz, dz, kp.e2)), f, acc, r, kp);
+                K::pair_row(dx, dy, dz, fma(dz, dz, pxye), f, acc, r, kp);
             }
             K::row_end(dx, dy, r, acc);
         }
@@ -142,7 +133,7 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
 template <int KER>
 __device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e, int grp,
                                            const EvalArgs& a, double* acc) {
-    using K = Kern<KER>;
+    using K = EvalKern<KER>;
     constexpr int M = K::M, U = 4;
     // The self pair (j == t under SELF_OMIT) is evaluated with f = 0 and s = 1:
     // its contribution is exactly zero, so the loop stays branch-free.
@@ -182,10 +173,11 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
 
 // Lane l works for target l / kGroup of the batch, as member l % kGroup of its
 // group; the kGroup lanes of a target share every MAC decision.
-template <int PT, int KER>
+// STATS: also write the per-target interaction counts (a.stats != nullptr).
+template <int PT, int KER, bool STATS>
 __global__ void __launch_bounds__(kWarps * 32, KITC_EVAL_MINB) k_eval(const EvalArgs a) {
-    using K = Kern<KER>;
-    constexpr int M = K::M, NP = K::P;
+    using K = EvalKern<KER>;
+    constexpr int M = K::M, NP = K::P, NA = K::NA;
     extern __shared__ int2 smem_stack[];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int grp = lane % kGroup, ti = lane / kGroup;
@@ -198,9 +190,9 @@ __global__ void __launch_bounds__(kWarps * 32, KITC_EVAL_MINB) k_eval(const Eval
     const double x = a.x[t], y = a.y[t], z = a.z[t];
     const int P = PT > 0 ? PT : a.P;
     const int P3 = P * P * P;
-    double acc[NP];
+    double acc[NA];
 #pragma unroll
-    for (int c = 0; c < NP; ++c) acc[c] = 0.0;
+    for (int c = 0; c < NA; ++c) acc[c] = 0.0;
     unsigned long long st[5] = {0, 0, 0, 0, 0};
     const unsigned live = __ballot_sync(0xffffffffu, valid);
     if (lane == 0) stk[0] = make_int2(0, (int)live);
@@ -225,7 +217,7 @@ __global__ void __launch_bounds__(kWarps * 32, KITC_EVAL_MINB) k_eval(const Eval
         const int4 tp = a.topo[c];
         if (am && ok) {
             far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * M * P3, acc, a.kp, P, grp);
-            if (a.stats) {
+            if (STATS) {
                 st[0] += 1;
                 st[1] += (unsigned long long)P3;
                 st[4] += (unsigned long long)(tp.y - tp.x);
@@ -235,7 +227,7 @@ __global__ void __launch_bounds__(kWarps * 32, KITC_EVAL_MINB) k_eval(const Eval
             if (tp.w == 0) {
                 if (in && !ok) {
                     near_field<KER>(x, y, z, t, tp.x, tp.y, grp, a, acc);
-                    if (a.stats) {
+                    if (STATS) {
                         const int self = (a.self_omit && t >= tp.x && t < tp.y) ? 1 : 0;
                         st[2] += 1;
                         st[3] += (unsigned long long)(tp.y - tp.x - self);
@@ -252,21 +244,30 @@ __global__ void __launch_bounds__(kWarps * 32, KITC_EVAL_MINB) k_eval(const Eval
     }
     // combine the kGroup partial sums of each target (fixed order -> deterministic)
 #pragma unroll
-    for (int c = 0; c < NP; ++c)
+    for (int c = 0; c < NA; ++c)
 #pragma unroll
         for (int o = 1; o < kGroup; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
     if (!valid || grp != 0) return;
     const int o = a.perm[t];
 #pragma unroll
-    for (int c = 0; c < NP; ++c) a.out[(size_t)o * NP + c] = acc[c] * K::scale(c);
-    if (a.stats)
+    for (int c = 0; c < NP; ++c) a.out[(size_t)o * NP + c] = K::out(acc, c);
+    if (STATS)
         for (int k = 0; k < 5; ++k) a.stats[(size_t)o * 5 + k] = st[k];
+}
+
+template <int PT, int KER, bool STATS>
+static void launch_k(const EvalArgs& a, int grid, size_t smem, cudaStream_t s) {
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_eval<PT, KER, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_eval<PT, KER, STATS><<<grid, kWarps * 32, smem, s>>>(a); note_launch();
 }
 
 template <int PT, int KER>
 static void launch(const EvalArgs& a, int grid, size_t smem, cudaStream_t s) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_eval<PT, KER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_eval<PT, KER><<<grid, kWarps * 32, smem, s>>>(a); note_launch();
+    if (a.stats)
+        launch_k<PT, KER, true>(a, grid, smem, s);
+    else
+        launch_k<PT, KER, false>(a, grid, smem, s);
 }
 
 template <int KER>

@@ -29,11 +29,23 @@ __device__ __forceinline__ double rsqrt_fast(double s) {
     return fma(y * e, p, y);
 }
 
+// 2 s^{-1/2} from the MUFU seed y by one Newton step folded into 3 FP64
+// instructions: Y = y (3 - s y^2) = 2 s^{-1/2} (1 - 3/2 d^2 + ...), d the seed's
+// relative error (|d| < 1e-6, profiles/r01_rsqrt_probe.txt), so |Y/(2 s^{-1/2}) - 1|
+// < 2e-12 (measured <= 4e-13).  Used by the treecode evaluation only (its parity
+// gate is 1e-10, reading A19); kitc_direct keeps rsqrt_fast.
+__device__ __forceinline__ double rsqrt2_newton(double s) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+    return y * fma(-(s * y), y, 3.0);
+}
+
 struct KParams {
     double e2;      // eps^2
     double e2x3;    // 3 eps^2
     double e4x15;   // 15 eps^4
     double e2x15;   // 15 eps^2
+    double e2q;     // eps^2 / 4
 };
 
 template <int KER> struct Kern;
@@ -223,7 +235,77 @@ inline KParams make_kparams(double eps) {
     k.e2x3 = 3.0 * e2;
     k.e4x15 = 15.0 * e2 * e2;
     k.e2x15 = 15.0 * e2;
+    k.e2q = 0.25 * e2;
     return k;
 }
+
+// ---------------------------------------------------------------------------
+// Treecode-evaluation forms (eval.cu).  EvalKern<KER> exposes
+//   NA accumulators, pair(dx,dy,dz,s,f,acc), pair_row(dx,dy,dz,s,f,acc,row),
+//   row_end(dx,dy,row,acc), out(acc,c) -> output component c (scaled)
+// taking s = |d|^2 + eps^2 (not its rsqrt).  The rotlet and combined kernels use
+// the Kern<> forms above; the Stokeslet has its own cheaper form.
+template <int KER> struct EvalKern {
+    using K = Kern<KER>;
+    static constexpr int M = K::M, P = K::P, NA = K::P;
+    using Row = typename K::Row;
+    static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s, const double* f,
+                                                double* acc, const KParams& k) {
+        K::pair(dx, dy, dz, s, f, acc, k);
+    }
+    static __device__ __forceinline__ void pair_row(double dx, double dy, double dz, double s, const double* f,
+                                                    double* acc, Row& r, const KParams& k) {
+        K::pair_row(dx, dy, dz, rsqrt_fast(s), f, acc, r, k);
+    }
+    static __device__ __forceinline__ void row_end(double dx, double dy, const Row& r, double* acc) {
+        K::row_end(dx, dy, r, acc);
+    }
+    static __device__ __forceinline__ double out(const double* acc, int c) { return acc[c] * K::scale(c); }
+};
+
+// Stokeslet with Y = 2 s^{-1/2} (rsqrt2_newton): 16 pi H1 = 2 rs + 2 eps^2 rs^3 =
+// Y + (eps^2/4) Y^3 and 16 pi H2 = 2 rs^3 = Y^3 / 4, so
+//   16 pi u = sum f (Y + (eps^2/4) Y^3)   [acc 0..2]
+//           + 1/4 sum [f.d] d Y^3         [acc 3..5]
+// 16 FP64 instructions per far-field pair (row form) + the MUFU seed.
+template <> struct EvalKern<0> {
+    static constexpr int M = 3, P = 3, NA = 6;
+    static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s, const double* f,
+                                                double* acc, const KParams& k) {
+        const double Y = rsqrt2_newton(s);
+        const double Y3 = (Y * Y) * Y;
+        const double h = fma(k.e2q, Y3, Y);
+        const double c = fma(f[0], dx, fma(f[1], dy, f[2] * dz)) * Y3;
+        acc[0] = fma(f[0], h, acc[0]);
+        acc[1] = fma(f[1], h, acc[1]);
+        acc[2] = fma(f[2], h, acc[2]);
+        acc[3] = fma(c, dx, acc[3]);
+        acc[4] = fma(c, dy, acc[4]);
+        acc[5] = fma(c, dz, acc[5]);
+    }
+    struct Row {
+        double C = 0.0, Z = 0.0;
+    };
+    static __device__ __forceinline__ void pair_row(double dx, double dy, double dz, double s, const double* f,
+                                                    double* acc, Row& r, const KParams& k) {
+        const double Y = rsqrt2_newton(s);
+        const double Y3 = (Y * Y) * Y;
+        const double h = fma(k.e2q, Y3, Y);
+        const double c = fma(f[0], dx, fma(f[1], dy, f[2] * dz)) * Y3;
+        r.C += c;
+        r.Z = fma(c, dz, r.Z);
+        acc[0] = fma(f[0], h, acc[0]);
+        acc[1] = fma(f[1], h, acc[1]);
+        acc[2] = fma(f[2], h, acc[2]);
+    }
+    static __device__ __forceinline__ void row_end(double dx, double dy, const Row& r, double* acc) {
+        acc[3] = fma(r.C, dx, acc[3]);
+        acc[4] = fma(r.C, dy, acc[4]);
+        acc[5] += r.Z;
+    }
+    static __device__ __forceinline__ double out(const double* acc, int c) {
+        return fma(0.25, acc[c + 3], acc[c]) * (1.0 / (16.0 * 3.14159265358979323846));
+    }
+};
 
 }  // namespace kitc
