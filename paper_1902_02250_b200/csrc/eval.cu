@@ -28,9 +28,21 @@ namespace {
 #define KITC_EVAL_WARPS 4
 #endif
 #ifndef KITC_EVAL_MINB
-#define KITC_EVAL_MINB 6
+#define KITC_EVAL_MINB 6  // resident CTAs per SM (register budget), Stokeslet
+#endif
+#ifndef KITC_EVAL_MINB1
+#define KITC_EVAL_MINB1 4  // rotlet / combined (measured: 4 beats 5 and 6 on C4)
+#endif
+#ifndef KITC_EVAL_PREFETCH
+#define KITC_EVAL_PREFETCH 0  // bit 0: far-field rows, bit 1: near-field sources
 #endif
 constexpr int kWarps = KITC_EVAL_WARPS;  // warps (batches) per CTA
+
+// L1 prefetch of one line (the next round's fhat rows / near-field sources, so
+// the loads of that round hit L1 instead of waiting on L2).
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 
 struct EvalArgs {
     const double* x;
@@ -87,6 +99,12 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
             if (nrow < full) {
                 gx = __ldg(g + nrow / PT);
                 gy = __ldg(g + PT + nrow % PT);
+                if (KITC_EVAL_PREFETCH & 1) {
+                    // the next round's kGroup rows of the P * M planes: 64 B each
+                    const double* nb = F + (nrow - grp);
+#pragma unroll
+                    for (int q = grp; q < PT * M; q += kGroup) prefetch_l1(nb + q * P2);
+                }
             }
             const double pxye = fma(dy, dy, dx * dx) + kp.e2;
             typename K::Row r;
@@ -140,6 +158,17 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
     const int self = a.self_omit ? t : -1;
     int j = b + grp;
     for (; j + (U - 1) * kGroup < e; j += U * kGroup) {
+        if (KITC_EVAL_PREFETCH & 2) {
+            // next iteration's U * kGroup sources: 2 lines of 128 B in each of 3 + M arrays
+            const int nj = j - grp + U * kGroup + 16 * (grp & 1);
+            const int arr = grp >> 1;  // 0..3
+            const double* base = arr == 0 ? a.x : arr == 1 ? a.y : arr == 2 ? a.z : a.w;
+            if (nj < e) {
+                prefetch_l1(base + nj);
+                if (arr == 3)
+                    for (int m = 1; m < M; ++m) prefetch_l1(a.w + (size_t)m * a.N + nj);
+            }
+        }
         double sx[U], sy[U], sz[U], f[U][M];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -175,7 +204,7 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
 // group; the kGroup lanes of a target share every MAC decision.
 // STATS: also write the per-target interaction counts (a.stats != nullptr).
 template <int PT, int KER, bool STATS>
-__global__ void __launch_bounds__(kWarps * 32, KITC_EVAL_MINB) k_eval(const EvalArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_EVAL_MINB1) k_eval(const EvalArgs a) {
     using K = EvalKern<KER>;
     constexpr int M = K::M, NP = K::P, NA = K::NA;
     extern __shared__ int2 smem_stack[];

@@ -46,6 +46,9 @@ struct KParams {
     double e4x15;   // 15 eps^4
     double e2x15;   // 15 eps^2
     double e2q;     // eps^2 / 4
+    double e2x3_8;  // 3 eps^2 / 8
+    double e4x15_32;  // 15 eps^4 / 32
+    double e2x5_8;  // 5 eps^2 / 8
 };
 
 template <int KER> struct Kern;
@@ -236,6 +239,9 @@ inline KParams make_kparams(double eps) {
     k.e4x15 = 15.0 * e2 * e2;
     k.e2x15 = 15.0 * e2;
     k.e2q = 0.25 * e2;
+    k.e2x3_8 = 0.375 * e2;
+    k.e4x15_32 = (15.0 / 32.0) * e2 * e2;
+    k.e2x5_8 = 0.625 * e2;
     return k;
 }
 
@@ -305,6 +311,79 @@ template <> struct EvalKern<0> {
     }
     static __device__ __forceinline__ double out(const double* acc, int c) {
         return fma(0.25, acc[c + 3], acc[c]) * (1.0 / (16.0 * 3.14159265358979323846));
+    }
+};
+
+// Rotlet with Y = 2 s^{-1/2}: rs^3 = Y^3/8, rs^5 = Y^5/32, rs^7 = Y^7/128, so
+//   q  = Y^3 + (3 eps^2/8) Y^5       = 4 (8 pi Q)
+//   d1 = (15 eps^4/32) Y^7 - q       = 4 (8 pi D1)
+//   d2 = Y^5 + (5 eps^2/8) Y^7       = (16/3) (8 pi D2)
+//   64 pi u  = sum [g x d] q                          [acc 0..2]
+//   128 pi w = sum g d1  [acc 3..5]  + 3/4 sum [g.d] d d2  [acc 6..8]
+// 26 FP64 instructions per far-field pair (row form) + the MUFU seed.
+template <> struct EvalKern<1> {
+    static constexpr int M = 3, P = 6, NA = 9;
+    static __device__ __forceinline__ void powers(double s, const KParams& k, double& q, double& d1, double& d2) {
+        const double Y = rsqrt2_newton(s);
+        const double Y2 = Y * Y;
+        const double Y3 = Y2 * Y;
+        const double Y5 = Y3 * Y2;
+        const double Y7 = Y5 * Y2;
+        q = fma(k.e2x3_8, Y5, Y3);
+        d1 = fma(k.e4x15_32, Y7, -q);
+        d2 = fma(k.e2x5_8, Y7, Y5);
+    }
+    static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s, const double* g,
+                                                double* acc, const KParams& k) {
+        double q, d1, d2;
+        powers(s, k, q, d1, d2);
+        const double cx = g[1] * dz - g[2] * dy;
+        const double cy = g[2] * dx - g[0] * dz;
+        const double cz = g[0] * dy - g[1] * dx;
+        acc[0] = fma(cx, q, acc[0]);
+        acc[1] = fma(cy, q, acc[1]);
+        acc[2] = fma(cz, q, acc[2]);
+        acc[3] = fma(g[0], d1, acc[3]);
+        acc[4] = fma(g[1], d1, acc[4]);
+        acc[5] = fma(g[2], d1, acc[5]);
+        const double gd = fma(g[0], dx, fma(g[1], dy, g[2] * dz)) * d2;
+        acc[6] = fma(gd, dx, acc[6]);
+        acc[7] = fma(gd, dy, acc[7]);
+        acc[8] = fma(gd, dz, acc[8]);
+    }
+    // row form (dx, dy fixed): sum q (g x d) = (B1 - dy A2, dx A2 - B0, dy A0 - dx A1)
+    // with A = sum q g, B = sum q dz g; sum (g.d) d2 d = (dx T, dy T, TZ).
+    struct Row {
+        double A0 = 0.0, A1 = 0.0, A2 = 0.0, B0 = 0.0, B1 = 0.0, T = 0.0, TZ = 0.0;
+    };
+    static __device__ __forceinline__ void pair_row(double dx, double dy, double dz, double s, const double* g,
+                                                    double* acc, Row& r, const KParams& k) {
+        double q, d1, d2;
+        powers(s, k, q, d1, d2);
+        r.A0 = fma(q, g[0], r.A0);
+        r.A1 = fma(q, g[1], r.A1);
+        r.A2 = fma(q, g[2], r.A2);
+        const double qz = q * dz;
+        r.B0 = fma(qz, g[0], r.B0);
+        r.B1 = fma(qz, g[1], r.B1);
+        acc[3] = fma(g[0], d1, acc[3]);
+        acc[4] = fma(g[1], d1, acc[4]);
+        acc[5] = fma(g[2], d1, acc[5]);
+        const double t = fma(g[0], dx, fma(g[1], dy, g[2] * dz)) * d2;
+        r.T += t;
+        r.TZ = fma(t, dz, r.TZ);
+    }
+    static __device__ __forceinline__ void row_end(double dx, double dy, const Row& r, double* acc) {
+        acc[0] += fma(-dy, r.A2, r.B1);
+        acc[1] += fma(dx, r.A2, -r.B0);
+        acc[2] += fma(dy, r.A0, -dx * r.A1);
+        acc[6] = fma(r.T, dx, acc[6]);
+        acc[7] = fma(r.T, dy, acc[7]);
+        acc[8] += r.TZ;
+    }
+    static __device__ __forceinline__ double out(const double* acc, int c) {
+        return c < 3 ? acc[c] * (1.0 / (64.0 * 3.14159265358979323846))
+                     : fma(0.75, acc[c + 3], acc[c]) * (1.0 / (128.0 * 3.14159265358979323846));
     }
 };
 
