@@ -190,10 +190,11 @@ def run_kitc(args, cfg, rank, world, local_rank):
     bshards = D.batch_shards(prefix, world) if world > 1 else [(0, T.nbatches)]
     cb, ce = cshards[rank]
     bb, be = bshards[rank]
-    gathered = torch.zeros((world, S, m, P3), dtype=torch.float64, device=dev)
-    fhat = torch.zeros((C, m, P3), dtype=torch.float64, device=dev)
+    L = kitc.kitc_fhat_cluster_len(kern, n)
+    gathered = torch.zeros((world, S, L), dtype=torch.float64, device=dev)
+    fhat = torch.zeros((C, L), dtype=torch.float64, device=dev)
     out = torch.zeros((N, p), dtype=torch.float64, device=dev)
-    row = m * P3 * 8
+    row = L * 8
     shard_base = gathered[rank].data_ptr() - cb * row    # virtual base: cluster c -> shard row c - cb
     import ctypes as Cc
 

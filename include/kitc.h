@@ -68,6 +68,11 @@ typedef struct kitc_tree kitc_tree; /* opaque, library-owned handle */
 /* Weight and output dimensions (m, p) of a kernel.  EINVAL for unknown k. */
 kitc_status kitc_kernel_dims(int32_t kernel, int32_t* m, int32_t* p);
 
+/* Doubles per cluster in the fhat layout of kernel k at degree n in [1, 16]
+ * (see kitc_modified_weights): R (n+1) m 8 with R = ceil((n+1)^2 / 8).
+ * EINVAL for unknown k or n out of range. */
+kitc_status kitc_fhat_cluster_len(int32_t kernel, int32_t n, int64_t* len);
+
 /* Create an empty tree handle (no device memory yet).  *out = NULL on error. */
 kitc_status kitc_tree_create(kitc_tree** out);
 
@@ -109,10 +114,14 @@ kitc_status kitc_tree_export(const kitc_tree* t, int64_t* perm_host, int64_t* be
  * exactly), simple weights (-1)^k delta_k, and the coincidence flag
  * |y - s_k| <= DBL_MIN -> L = e_k (last k wins).
  *  w_dev: device, double[N][m] in ORIGINAL order (m from kitc_kernel_dims).
- *  fhat_dev: device, double[C][(n+1)^3 m] in the order [c][k3][comp][k1 (n+1) + k2]
- *  (per cluster: n+1 planes of m components, each holding the (n+1)^2 rows
- *  (k1, k2) contiguously); only the requested clusters' slices are written.  Also gathers w into the tree's sorted
- *  layout and computes every cluster's grid (both used by kitc_eval).
+ *  fhat_dev: device, 16-byte aligned, double[C][L] with L from
+ *  kitc_fhat_cluster_len, in the order [c][r][k3][comp][j]: the (n+1)^2 rows
+ *  row = k1 (n+1) + k2 = 8 r + j are grouped in blocks of 8 ("rounds"), each
+ *  block holding all k3 and components of its 8 rows contiguously (one bulk
+ *  copy per round in kitc_eval); rows >= (n+1)^2 of the last block are written
+ *  as 0.  Only the requested clusters' slices are written (a contiguous byte
+ *  range per cluster range).  Also gathers w into the tree's sorted layout and
+ *  computes every cluster's grid (both used by kitc_eval).
  *  0 <= cluster_begin <= cluster_end <= C.  ESTATE if no tree is built. */
 kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const double* w_dev,
                                   int64_t cluster_begin, int64_t cluster_end, double* fhat_dev,
@@ -127,7 +136,8 @@ kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const
  * rejected internal -> children.
  *  n, kernel: must match the last kitc_modified_weights call; N0 must equal
  *  the tree's N0; 0 <= theta < 1; eps >= 0 (eps = 0 requires SELF_OMIT).
- *  fhat_dev: the FULL double[C][(n+1)^3 m] of kitc_modified_weights (every cluster).
+ *  fhat_dev: the FULL double[C][L] of kitc_modified_weights (every cluster),
+ *  16-byte aligned (else EINVAL).
  *  out_dev: device double[N][p], original order; only the targets of the given
  *  batches are written.
  *  stats_dev: optional (NULL = off) device uint64[N][5], original order:

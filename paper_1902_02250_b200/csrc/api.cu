@@ -18,6 +18,14 @@ using namespace kitc;
 
 extern "C" {
 
+kitc_status kitc_fhat_cluster_len(int32_t kernel, int32_t n, int64_t* len) {
+    int32_t m = 0;
+    KITC_TRY(kitc_kernel_dims(kernel, &m, nullptr));
+    if (n < 1 || n > kitc::kMaxDegree) return kitc::set_error(KITC_EINVAL, "kitc_fhat_cluster_len: n must be in [1, 16]");
+    if (len) *len = kitc::fhat_cluster_len(n + 1, m);
+    return KITC_OK;
+}
+
 kitc_status kitc_kernel_dims(int32_t kernel, int32_t* m, int32_t* p) {
     int mm, pp;
     switch (kernel) {

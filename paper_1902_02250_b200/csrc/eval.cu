@@ -28,21 +28,18 @@ namespace {
 #define KITC_EVAL_WARPS 4
 #endif
 #ifndef KITC_EVAL_MINB
-#define KITC_EVAL_MINB 6  // resident CTAs per SM (register budget), Stokeslet
+#define KITC_EVAL_MINB 4  // resident CTAs per SM (register budget), Stokeslet (measured: 4 > 5 > 6, 3)
 #endif
 #ifndef KITC_EVAL_MINB1
 #define KITC_EVAL_MINB1 4  // rotlet / combined (measured: 4 beats 5 and 6 on C4)
 #endif
-#ifndef KITC_EVAL_PREFETCH
-#define KITC_EVAL_PREFETCH 0  // bit 0: far-field rows, bit 1: near-field sources
+#ifndef KITC_EVAL_SB
+#define KITC_EVAL_SB 2
 #endif
 constexpr int kWarps = KITC_EVAL_WARPS;  // warps (batches) per CTA
-
-// L1 prefetch of one line (the next round's fhat rows / near-field sources, so
-// the loads of that round hit L1 instead of waiting on L2).
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
+constexpr int kSB = KITC_EVAL_SB;         // fhat blocks per pipeline stage (1 or 2)
+static_assert(kSB == 1 || kSB == 2, "kSB");
+static_assert(kGroup == kRows, "k_eval: one fhat row per lane of a target group");
 
 struct EvalArgs {
     const double* x;
@@ -63,87 +60,171 @@ struct EvalArgs {
     int N;
     int P;  // n + 1 (runtime copy)
     int stack_cap;
+    int warp_smem;  // bytes of shared memory per warp (WarpSmem)
     int self_omit;
     double tt;  // theta * theta (RN)
     KParams kp;
 };
 
-// Far field of one accepted cluster for the lanes of one target group: lane
-// group g (of kGroup) sums rows (k1, k2) = g, g + kGroup, ... of the (n+1)^2
-// rows, all k3 per row (dx, dy, dx^2 + dy^2 per row and dz, dz^2 + eps^2 per
-// plane are reused; Kern::pair_row folds the terms linear in d along the row);
-// the rows left after the last full round are split pair by pair over the
-// groups.  F layout: F[k3][m][row], row = k1 (n+1) + k2 (weights.cu).
+// ---- per-warp shared memory: two fhat round buffers (TMA destinations), their
+// mbarriers, the number of rounds issued so far (-> buffer and phase parity of
+// the next round), and the DFS stack.
+struct WarpSmem {
+    double* buf;               // 2 x blk doubles
+    unsigned long long* bar;   // 2 mbarriers
+    int* nround;
+    int2* stk;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// One elected lane: arm the barrier with the byte count and start the bulk
+// copy global -> shared, which completes the transaction on the barrier.
+__device__ __forceinline__ void tma_round(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
+    const unsigned b = smem_u32(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "KITC_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra KITC_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Far field of one accepted cluster (Eq. pc_approximation_3D) for
+// the accepted lanes `am` of the warp.  fhat comes in blocks of kRows = 8 rows
+// (k1, k2) x all k3 x all m (weights.cu layout); kSB consecutive blocks form a
+// stage, staged into shared memory by ONE bulk copy two stages ahead of its use
+// (double buffer, mbarrier completion), so the FP64 work never waits on L2.
+// Every row is summed over all k3 with dx, dy, dx^2 + dy^2 + eps^2 per row and
+// dz per plane reused (EvalKern::pair_row folds the terms linear in d along the
+// row).  In a stage of two full blocks lane g of a target group takes the two
+// adjacent rows 2(g%4), 2(g%4)+1 of block g/4 (one 16-byte shared load fetches
+// both rows' weights; two independent pair chains); a stage with one full block
+// gives each lane one row; the rows of a partial last block are split pair by
+// pair over the lanes.
 template <int PT, int KER>
 __device__ __forceinline__ void far_field(double x, double y, double z, const double* __restrict__ g,
                                           const double* __restrict__ F, double* acc, const KParams& kp, int Prt,
-                                          int grp) {
+                                          int grp, int lane, unsigned am, const WarpSmem& ws) {
     using K = EvalKern<KER>;
     constexpr int M = K::M;
     const int P = PT > 0 ? PT : Prt, P2 = P * P;
-    const int full = (P2 / kGroup) * kGroup;
+    const int R = (P2 + kRows - 1) / kRows, RF = P2 / kRows;  // blocks, full blocks
+    const int blk = P * M * kRows;                            // doubles per block
+    const int NS = (R + kSB - 1) / kSB;                       // stages
+    const bool leader = lane == __ffs(am) - 1;
+    const int base = *ws.nround;
+    auto issue = [&](int st, int k) {  // stage st of this cluster -> buffer k & 1
+        const int nb = min(kSB, R - st * kSB);
+        tma_round(ws.buf + (k & 1) * kSB * blk, F + (size_t)st * kSB * blk, (unsigned)(nb * blk * 8),
+                  ws.bar + (k & 1));
+    };
+    if (leader) {
+        issue(0, base);
+        if (NS > 1) issue(1, base + 1);
+    }
+    double dz[PT > 0 ? PT : 1];
     if constexpr (PT > 0) {
-        double dz[PT];
 #pragma unroll
         for (int k3 = 0; k3 < PT; ++k3) dz[k3] = z - __ldg(g + 2 * PT + k3);
-        // the next row's grid coordinates are loaded one row ahead
-        double gx = 0.0, gy = 0.0;
-        if (grp < full) {
-            gx = __ldg(g + grp / PT);
-            gy = __ldg(g + PT + grp % PT);
-        }
-        for (int row = grp; row < full; row += kGroup) {
-            const double dx = x - gx;
-            const double dy = y - gy;
-            const int nrow = row + kGroup;
-            if (nrow < full) {
-                gx = __ldg(g + nrow / PT);
-                gy = __ldg(g + PT + nrow % PT);
-                if (KITC_EVAL_PREFETCH & 1) {
-                    // the next round's kGroup rows of the P * M planes: 64 B each
-                    const double* nb = F + (nrow - grp);
+    }
+    for (int st = 0; st < NS; ++st) {
+        const int k = base + st;
+        const double* B = ws.buf + (k & 1) * kSB * blk;
+        mbar_wait(ws.bar + (k & 1), (unsigned)(k >> 1) & 1u);
+        const int b0 = st * kSB;  // first block of the stage
+        if (kSB == 2 && b0 + 1 < RF) {
+            // two full blocks: rows ra, ra + 1 of block h = grp / 4
+            const int h = grp >> 2, j = 2 * (grp & 3);
+            const int ra = (b0 + h) * kRows + j;
+            const int k1a = ra / P, k2a = ra - k1a * P;
+            const int k1b = k2a + 1 == P ? k1a + 1 : k1a, k2b = k2a + 1 == P ? 0 : k2a + 1;
+            const double dxa = x - __ldg(g + k1a), dya = y - __ldg(g + P + k2a);
+            const double dxb = x - __ldg(g + k1b), dyb = y - __ldg(g + P + k2b);
+            const double pa = fma(dya, dya, dxa * dxa) + kp.e2;
+            const double pb = fma(dyb, dyb, dxb * dxb) + kp.e2;
+            const double* Bh = B + h * blk + j;
+            typename K::Row rA, rB;
+            if constexpr (PT > 0) {
 #pragma unroll
-                    for (int q = grp; q < PT * M; q += kGroup) prefetch_l1(nb + q * P2);
+                for (int k3 = 0; k3 < PT; ++k3) {
+                    double fa[M], fb[M];
+#pragma unroll
+                    for (int m = 0; m < M; ++m) {
+                        const double2 v = *reinterpret_cast<const double2*>(Bh + (k3 * M + m) * kRows);
+                        fa[m] = v.x;
+                        fb[m] = v.y;
+                    }
+                    K::pair_row(dxa, dya, dz[k3], fma(dz[k3], dz[k3], pa), fa, acc, rA, kp);
+                    K::pair_row(dxb, dyb, dz[k3], fma(dz[k3], dz[k3], pb), fb, acc, rB, kp);
+                }
+            } else {
+                for (int k3 = 0; k3 < P; ++k3) {
+                    const double dzk = z - __ldg(g + 2 * P + k3);
+                    double fa[M], fb[M];
+#pragma unroll
+                    for (int m = 0; m < M; ++m) {
+                        const double2 v = *reinterpret_cast<const double2*>(Bh + (k3 * M + m) * kRows);
+                        fa[m] = v.x;
+                        fb[m] = v.y;
+                    }
+                    K::pair_row(dxa, dya, dzk, fma(dzk, dzk, pa), fa, acc, rA, kp);
+                    K::pair_row(dxb, dyb, dzk, fma(dzk, dzk, pb), fb, acc, rB, kp);
                 }
             }
-            const double pxye = fma(dy, dy, dx * dx) + kp.e2;
-            typename K::Row r;
+            K::row_end(dxa, dya, rA, acc);
+            K::row_end(dxb, dyb, rB, acc);
+        } else {
+            for (int bb = b0; bb < min(b0 + kSB, R); ++bb) {
+                const double* Bb = B + (bb - b0) * blk;
+                if (bb < RF) {  // full block: one row per lane
+                    const int row = bb * kRows + grp;
+                    const int k1 = row / P, k2 = row - k1 * P;
+                    const double dx = x - __ldg(g + k1), dy = y - __ldg(g + P + k2);
+                    const double pxye = fma(dy, dy, dx * dx) + kp.e2;
+                    typename K::Row r;
+                    for (int k3 = 0; k3 < P; ++k3) {
+                        const double dzk = z - __ldg(g + 2 * P + k3);
+                        double f[M];
 #pragma unroll
-            for (int k3 = 0; k3 < PT; ++k3) {
-                double f[M];
+                        for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + grp];
+                        K::pair_row(dx, dy, dzk, fma(dzk, dzk, pxye), f, acc, r, kp);
+                    }
+                    K::row_end(dx, dy, r, acc);
+                } else {  // partial last block: pair by pair
+                    const int pairs = (P2 - RF * kRows) * P;
+                    for (int q = grp; q < pairs; q += kRows) {
+                        const int jj = q / P, k3 = q - jj * P, row = RF * kRows + jj;
+                        const int k1 = row / P, k2 = row - k1 * P;
+                        const double dx = x - __ldg(g + k1), dy = y - __ldg(g + P + k2),
+                                     dzk = z - __ldg(g + 2 * P + k3);
+                        double f[M];
 #pragma unroll
-                for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
-                K::pair_row(dx, dy, dz[k3], fma(dz[k3], dz[k3], pxye), f, acc, r, kp);
+                        for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + jj];
+                        K::pair(dx, dy, dzk, fma(dy, dy, dx * dx) + fma(dzk, dzk, kp.e2), f, acc, kp);
+                    }
+                }
             }
-            K::row_end(dx, dy, r, acc);
         }
-    } else {
-        for (int row = grp; row < full; row += kGroup) {
-            const int k1 = row / P, k2 = row - k1 * P;
-            const double dx = x - __ldg(g + k1);
-            const double dy = y - __ldg(g + P + k2);
-            const double pxye = fma(dy, dy, dx * dx) + kp.e2;
-            typename K::Row r;
-            for (int k3 = 0; k3 < P; ++k3) {
-                const double dz = z - __ldg(g + 2 * P + k3);
-                double f[M];
-#pragma unroll
-                for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
-                K::pair_row(dx, dy, dz, fma(dz, dz, pxye), f, acc, r, kp);
-            }
-            K::row_end(dx, dy, r, acc);
+        __syncwarp(am);  // every accepted lane is done with buffer k & 1
+        if (leader && st + 2 < NS) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(st + 2, k);
         }
     }
-    const int rem = (P2 - full) * P;  // pairs of the leftover rows
-    for (int q = grp; q < rem; q += kGroup) {
-        const int row = full + q / P, k3 = q - (q / P) * P;
-        const int k1 = row / P, k2 = row - k1 * P;
-        const double dx = x - __ldg(g + k1), dy = y - __ldg(g + P + k2), dz = z - __ldg(g + 2 * P + k3);
-        double f[M];
-#pragma unroll
-        for (int m = 0; m < M; ++m) f[m] = __ldg(F + (k3 * M + m) * P2 + row);
-        K::pair(dx, dy, dz, fma(dy, dy, dx * dx) + fma(dz, dz, kp.e2), f, acc, kp);
-    }
+    if (leader) *ws.nround = base + NS;
+    __syncwarp(am);
 }
 
 // Near field of one rejected leaf: lane group g sums sources b + g, b + g + kGroup, ...
@@ -158,17 +239,6 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
     const int self = a.self_omit ? t : -1;
     int j = b + grp;
     for (; j + (U - 1) * kGroup < e; j += U * kGroup) {
-        if (KITC_EVAL_PREFETCH & 2) {
-            // next iteration's U * kGroup sources: 2 lines of 128 B in each of 3 + M arrays
-            const int nj = j - grp + U * kGroup + 16 * (grp & 1);
-            const int arr = grp >> 1;  // 0..3
-            const double* base = arr == 0 ? a.x : arr == 1 ? a.y : arr == 2 ? a.z : a.w;
-            if (nj < e) {
-                prefetch_l1(base + nj);
-                if (arr == 3)
-                    for (int m = 1; m < M; ++m) prefetch_l1(a.w + (size_t)m * a.N + nj);
-            }
-        }
         double sx[U], sy[U], sz[U], f[U][M];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -207,10 +277,27 @@ template <int PT, int KER, bool STATS>
 __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_EVAL_MINB1) k_eval(const EvalArgs a) {
     using K = EvalKern<KER>;
     constexpr int M = K::M, NP = K::P, NA = K::NA;
-    extern __shared__ int2 smem_stack[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const int grp = lane % kGroup, ti = lane / kGroup;
-    int2* stk = smem_stack + wl * a.stack_cap;
+    WarpSmem ws;
+    {
+        const int P = PT > 0 ? PT : a.P;
+        const int blk = P * M * kRows;
+        unsigned char* base = smem_raw + (size_t)wl * a.warp_smem;
+        ws.buf = reinterpret_cast<double*>(base);
+        ws.bar = reinterpret_cast<unsigned long long*>(base + 2 * kSB * blk * sizeof(double));
+        ws.nround = reinterpret_cast<int*>(ws.bar + 2);
+        ws.stk = reinterpret_cast<int2*>(ws.bar + 3);
+        if (lane == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(ws.bar)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(ws.bar + 1)));
+            *ws.nround = 0;
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    int2* stk = ws.stk;
     const long long b = a.bb + (long long)blockIdx.x * kWarps + wl;
     if (b >= a.be) return;  // whole warp
     const int p0 = a.bstart[b], tc = a.bcount[b];
@@ -219,6 +306,7 @@ __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_
     const double x = a.x[t], y = a.y[t], z = a.z[t];
     const int P = PT > 0 ? PT : a.P;
     const int P3 = P * P * P;
+    const long long LEN = (long long)((P * P + kRows - 1) / kRows) * P * M * kRows;  // fhat doubles per cluster
     double acc[NA];
 #pragma unroll
     for (int c = 0; c < NA; ++c) acc[c] = 0.0;
@@ -245,7 +333,8 @@ __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_
         const unsigned rm = mask & ~am;
         const int4 tp = a.topo[c];
         if (am && ok) {
-            far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * M * P3, acc, a.kp, P, grp);
+            far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * LEN, acc, a.kp, P, grp,
+                               lane, am, ws);
             if (STATS) {
                 st[0] += 1;
                 st[1] += (unsigned long long)P3;
@@ -354,7 +443,13 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     a.self_omit = self == KITC_SELF_OMIT;
     a.tt = theta * theta;
     a.kp = make_kparams(eps);
-    const size_t smem = (size_t)kWarps * a.stack_cap * sizeof(int2);
+    int m = 0;
+    KITC_TRY(kitc_kernel_dims(kernel, &m, nullptr));
+    if (reinterpret_cast<uintptr_t>(fhat) % 16) return set_error(KITC_EINVAL, "kitc_eval: fhat must be 16-byte aligned");
+    // per warp: 2 stage buffers + 2 mbarriers + round counter (8 B) + stack, 128-B multiple
+    a.warp_smem = (int)(((size_t)2 * kSB * (n + 1) * m * kRows * sizeof(double) + 24 + (size_t)a.stack_cap * sizeof(int2) +
+                         127) / 128 * 128);
+    const size_t smem = (size_t)kWarps * a.warp_smem;
     if (smem > 200 * 1024) return set_error(KITC_EINVAL, "kitc_eval: tree too deep for the traversal stack");
     const long long nb = be - bb;
     const int grid = (int)((nb + kWarps - 1) / kWarps);

@@ -19,6 +19,11 @@ constexpr int kGroup = KITC_GROUP;    // lanes cooperating on one target in k_ev
 constexpr int kBatch = 32 / kGroup;   // targets per warp batch
 constexpr double kPi = 3.14159265358979323846;
 
+// fhat layout (include/kitc.h): per cluster [r][k3][m][j], row = k1 P + k2 = kRows r + j.
+constexpr int kRows = 8;  // rows per round block = lanes per target in k_eval
+inline int fhat_rounds(int P) { return (P * P + kRows - 1) / kRows; }
+inline long long fhat_cluster_len(int P, int M) { return (long long)fhat_rounds(P) * P * M * kRows; }
+
 extern std::atomic<unsigned long long> g_launches;  // kernels launched by the library
 inline void note_launch(unsigned long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 

@@ -8,9 +8,9 @@
 // last k wins) and stages them with the weights in shared memory; phase 2 has
 // thread (k2, k3) accumulate fhat[m][k1][k2][k3] += Lx[k1] (Ly[k2] Lz[k3] f_m)
 // in registers for all k1 and m (the tensor-product loop of lines 20-22).
-// Layout (include/kitc.h): fhat[c][k3][m][k1 (n+1) + k2] -- the (n+1)^2 rows
-// (k1, k2) of one (k3, m) plane are contiguous, so the kGroup lane groups of
-// k_eval, which take consecutive rows, read one contiguous segment per load.
+// Layout (include/kitc.h): fhat[c][r][k3][m][j], row = k1 (n+1) + k2 = 8 r + j:
+// blocks of 8 rows ("rounds") hold all k3 and m of those rows contiguously, so
+// k_eval stages one round with one bulk copy; padding rows of the last round are 0.
 // Chunks of one cluster write partials that a second kernel sums in chunk
 // order (deterministic).  Reading A15: L per axis instead of
 // (a1 a2 a3 / denom) -- rounding-only difference.
@@ -92,7 +92,8 @@ __global__ void __launch_bounds__((P * P + 31) / 32 * 32) k_weights(
     const WItem* __restrict__ items, const double* __restrict__ x, const double* __restrict__ y,
     const double* __restrict__ z, const double* __restrict__ ws, int N, const double* __restrict__ grid,
     double* __restrict__ fhat, double* __restrict__ part) {
-    constexpr int P2 = P * P, P3 = P2 * P, NT = (P2 + 31) / 32 * 32;
+    constexpr int P2 = P * P, NT = (P2 + 31) / 32 * 32, R = (P2 + kRows - 1) / kRows;
+    constexpr int LEN = R * P * M * kRows;
     __shared__ double sg[3 * P];
     __shared__ double Lx[kTile][P], Ly[kTile][P], Lz[kTile][P], sw[kTile][M];
     const WItem it = items[blockIdx.x];
@@ -130,12 +131,20 @@ __global__ void __launch_bounds__((P * P + 31) / 32 * 32) k_weights(
         }
         __syncthreads();
     }
+    double* dst = it.slot < 0 ? fhat + (size_t)it.c * LEN : part + (size_t)it.slot * LEN;
+    // zero padding rows P2 .. R kRows - 1
+    for (int q = tid; q < (R * kRows - P2) * P * M; q += NT) {
+        const int row = P2 + q / (P * M), km = q % (P * M);
+        dst[((row / kRows) * P * M + km) * kRows + row % kRows] = 0.0;
+    }
     if (!owner) return;
-    double* dst = it.slot < 0 ? fhat + (size_t)it.c * M * P3 : part + (size_t)it.slot * M * P3;
 #pragma unroll
     for (int m = 0; m < M; ++m)
 #pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) dst[(k3 * M + m) * P2 + k1 * P + k2] = acc[m][k1];
+        for (int k1 = 0; k1 < P; ++k1) {
+            const int row = k1 * P + k2;
+            dst[(((row / kRows) * P + k3) * M + m) * kRows + row % kRows] = acc[m][k1];
+        }
 }
 
 struct RItem {
@@ -185,7 +194,8 @@ kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, i
     if (!t->built) return set_error(KITC_ESTATE, "kitc_modified_weights: tree not built");
     if (cb < 0 || ce > t->nclusters || cb > ce) return set_error(KITC_EINVAL, "kitc_modified_weights: bad cluster range");
     if (!w || (!fhat && ce > cb)) return set_error(KITC_EINVAL, "kitc_modified_weights: NULL buffer");
-    const int N = (int)t->N, C = (int)t->nclusters, P = n + 1, P3 = P * P * P;
+    const int N = (int)t->N, C = (int)t->nclusters, P = n + 1;
+    const long long LEN = fhat_cluster_len(P, m);
     // sorted weights (SoA, m planes)
     KITC_TRY(t->w.ensure((size_t)m * N * sizeof(double), s));
     k_gather_w<<<(N + 255) / 256, 256, 0, s>>>(w, t->perm.as<int>(), N, m, t->w.as<double>()); note_launch();
@@ -222,7 +232,7 @@ kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, i
     std::copy(red.begin(), red.end(), reinterpret_cast<RItem*>(t->h_stage.as<char>() + o1));
     KITC_TRY(t->d_witems.ensure(o2, s));
     KITC_CUDA(cudaMemcpyAsync(t->d_witems.p, t->h_stage.p, o2, cudaMemcpyHostToDevice, s));
-    KITC_TRY(t->d_wpart.ensure((size_t)std::max(nslots, 1) * m * P3 * sizeof(double), s));
+    KITC_TRY(t->d_wpart.ensure((size_t)std::max(nslots, 1) * LEN * sizeof(double), s));
     const WItem* di = t->d_witems.as<WItem>();
     if (m == 3)
         KITC_TRY(dispatch<3>(n, (int)items.size(), di, t, t->w.as<double>(), t->grid.as<double>(), fhat,
@@ -232,7 +242,7 @@ kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, i
                              t->d_wpart.as<double>(), s));
     if (!red.empty())
         k_reduce<<<(int)red.size(), 256, 0, s>>>(reinterpret_cast<const RItem*>(t->d_witems.as<char>() + o1),
-                                                 m * P3, t->d_wpart.as<double>(), fhat); note_launch();
+                                                 (int)LEN, t->d_wpart.as<double>(), fhat); note_launch();
     KITC_CUDA(cudaGetLastError());
     return KITC_OK;
 }

@@ -27,7 +27,7 @@ SELF_OMIT, SELF_INCLUDE = 0, 1
 KERNELS = {"stokeslet": STOKESLET, "rotlet": ROTLET, "stokeslet_rotlet": STOKESLET_ROTLET}
 
 # every symbol include/kitc.h declares
-EXPORTS = ("kitc_kernel_dims", "kitc_tree_create", "kitc_build_tree", "kitc_tree_info",
+EXPORTS = ("kitc_kernel_dims", "kitc_fhat_cluster_len", "kitc_tree_create", "kitc_build_tree", "kitc_tree_info",
            "kitc_tree_export", "kitc_modified_weights", "kitc_eval", "kitc_batch_targets",
            "kitc_direct", "kitc_rel_error", "kitc_tree_free", "kitc_last_error",
            "kitc_launch_count")
@@ -109,6 +109,12 @@ def kitc_kernel_dims(kernel):
     return m.value, p.value
 
 
+def kitc_fhat_cluster_len(kernel, n):
+    ln = C.c_int64()
+    _call("kitc_fhat_cluster_len", int(kernel), int(n), C.byref(ln))
+    return ln.value
+
+
 def kitc_tree_create():
     h = C.c_void_p()
     _call("kitc_tree_create", C.byref(h))
@@ -183,8 +189,8 @@ class Tree:
         return self._h
 
     def fhat_shape(self, kernel, n):
-        m, _ = kitc_kernel_dims(kernel)
-        return (self.nclusters, m, (n + 1) ** 3)
+        """[C][L]: per cluster [round][k3][comp][8 rows] (include/kitc.h)."""
+        return (self.nclusters, kitc_fhat_cluster_len(kernel, n))
 
     def modified_weights(self, kernel, n, W, cluster_range=None, fhat=None, stream=None):
         m, _ = kitc_kernel_dims(kernel)

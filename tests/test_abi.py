@@ -74,3 +74,16 @@ def test_validation_without_gpu():
         kitc.kitc_tree_info(h)                                # not built
     assert e.value.status == kitc.KITC_ESTATE
     kitc.kitc_tree_free(h)
+
+
+def test_fhat_cluster_len(lib):
+    # [round][k3][comp][8 rows], rounds = ceil((n+1)^2 / 8)  (include/kitc.h)
+    ln = C.c_int64()
+    for kern, m in ((0, 3), (1, 3), (2, 6)):
+        for n in (1, 4, 8, 16):
+            P = n + 1
+            assert lib.kitc_fhat_cluster_len(kern, n, C.byref(ln)) == 0
+            assert ln.value == -(-P * P // 8) * P * m * 8
+    assert lib.kitc_fhat_cluster_len(0, 0, C.byref(ln)) == -1
+    assert lib.kitc_fhat_cluster_len(0, 17, C.byref(ln)) == -1
+    assert lib.kitc_fhat_cluster_len(7, 4, C.byref(ln)) == -1

@@ -35,12 +35,17 @@ def host(t):
     return t.cpu().numpy()
 
 
-def fhat_to_oracle(F, n):
-    """GPU fhat [C][k3][m][k1 (n+1) + k2] -> oracle [C][m][(k1 (n+1) + k2) (n+1) + k3]."""
+def fhat_to_oracle(F, n, pad_zero=True):
+    """GPU fhat [C][r][k3][m][j] (row = k1 (n+1) + k2 = 8 r + j, include/kitc.h)
+    -> oracle [C][m][(k1 (n+1) + k2) (n+1) + k3].  Checks the padding rows are 0."""
     P = n + 1
+    R = (P * P + 7) // 8
     C = F.shape[0]
-    m = F.size // (C * P ** 3)
-    return np.ascontiguousarray(F.reshape(C, P, m, P, P).transpose(0, 2, 3, 4, 1)).reshape(C, m, P ** 3)
+    m = F.size // (C * R * P * 8)
+    G = F.reshape(C, R, P, m, 8).transpose(0, 3, 1, 4, 2).reshape(C, m, R * 8, P)
+    if pad_zero:
+        assert not G[:, :, P * P:, :].any(), "fhat padding rows must be written as 0"
+    return np.ascontiguousarray(G[:, :, : P * P, :]).reshape(C, m, P ** 3)
 
 
 # ---------------------------------------------------------------- direct sum
