@@ -130,6 +130,9 @@ def run_gpu(K, X, W, kern, n, theta, N0, eps, self_omit=True):
     (7000, 80, 3, 0.5, 0, 0.01, "slab"),
     (3000, 30, 12, 0.7, 0, 0.01, "uniform"),      # generic (runtime-P) kernel
     (600, 20, 2, 0.0, 0, 0.01, "uniform"),        # theta = 0 -> direct
+    (2999, 37, 4, 0.7, 0, 0.01, "uniform"),       # odd N, odd leaf bounds: pad source at index N
+    (1001, 19, 7, 0.7, 1, 0.02, "sphere"),        # odd N, rotlet, partial last fhat block
+    (3, 1, 1, 0.7, 0, 0.01, "uniform"),           # tiny: one-particle leaves
 ])
 def test_treecode_parity(K, N, N0, n, theta, kern, eps, geom):
     m = O.DIMS[kern][0]
