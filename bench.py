@@ -304,8 +304,16 @@ def run_kitc(args, cfg, rank, world, local_rank):
     smax = float(peaks.get("sm_max_mhz", 1965.0))
     peak_tflops = PEAK_SMS * PEAK_FMA_PER_CLK * 2 * smax * 1e6 / 1e12
     achieved = flops_eval / (eval_launch_ms * 1e-3) / 1e12
+    traffic, traffic_src = None, None
+    try:  # dram read + write bytes of one k_eval launch from the committed ncu --set full capture
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[args.config]
+        traffic, traffic_src = tr["dram_bytes_per_launch"], tr["source"]
+    except Exception:
+        pass
     roof = {"bound": "alu", "kernel": "k_eval (treecode evaluation)", "achieved": achieved,
-            "peak": peak_tflops, "unit": "TFLOP/s", "frac": achieved / peak_tflops, "traffic": None,
+            "peak": peak_tflops, "unit": "TFLOP/s", "frac": achieved / peak_tflops, "traffic": traffic,
+            "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+            "traffic_source": traffic_src,
             "peak_source": f"derived: {PEAK_SMS} SMs x {PEAK_FMA_PER_CLK} FP64 FMA/clk x 2 x {smax:.0f} MHz "
                            "(DFMA probe measured 34.1 TFLOP/s, profiles/r01_fp64_peak.txt)",
             "algorithmic_flops_per_launch": flops_eval, "pairs_per_launch": pairs,
@@ -322,7 +330,7 @@ def run_kitc(args, cfg, rank, world, local_rank):
     line = {"metric": metric_for(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (kitc_inputs: uniform [-1,1]^3, seed 0)",
+            "data": f"synthetic (kitc_inputs: {cfg['geometry']}, weights uniform [-1,1]^m, seed 0)",
             "config": {"workload": f"{args.config} ({KI.CONFIGS[args.config]})",
                        "parallelism": f"tree replicated, fhat sharded + NCCL all-gather, targets dp{world}",
                        "l2": "flushed between timed steps (256 MB write, untimed)",
