@@ -57,6 +57,8 @@ def lib():
         L.orc_modified_weights_box.argtypes = [i64, vp, vp, i32, i32, vp, vp, vp]
         L.orc_treecode.argtypes = [vp, i32, d, i32, d, i32, vp, vp, vp, i64, vp, vp]
         L.orc_direct.argtypes = [i32, d, i32, i32, i64, vp, vp, vp, i64, vp]
+        L.orc_treecode_targets.argtypes = [vp, i32, d, i32, d, vp, vp, vp, i64, vp, vp]
+        L.orc_direct_targets.argtypes = [i32, d, i32, i64, vp, vp, vp, i64, vp]
         L.orc_rel_error.argtypes = [vp, vp, i64, i32]
         L.orc_rel_error.restype = d
         _lib = L
@@ -180,6 +182,22 @@ class Tree:
         return (out, st) if stats else out
 
 
+    def treecode_targets(self, kernel, eps, n, theta, W, Xt, fhat=None, stats=False):
+        """Treecode at a separate target set Xt (nt x 3); no self term."""
+        m, p = DIMS[kernel]
+        W = _f64(W).reshape(self.N, m)
+        Xt = _f64(Xt).reshape(-1, 3)
+        if fhat is None:
+            fhat = self.modified_weights(W, n)
+        nt = Xt.shape[0]
+        out = np.empty((nt, p))
+        st = np.empty((nt, 5), np.uint64) if stats else None
+        rc = lib().orc_treecode_targets(self._h, kernel, float(eps), n, float(theta), _p(_f64(fhat)), _p(W),
+                                        _p(Xt), nt, _p(out), _p(st))
+        assert rc == 0
+        return (out, st) if stats else out
+
+
 def modified_weights_box(Y, Fw, n, lo, hi):
     Y, Fw = _f64(Y).reshape(-1, 3), _f64(Fw)
     Fw = Fw.reshape(Y.shape[0], -1)
@@ -201,6 +219,19 @@ def direct(kernel, eps, X, W, targets=None, self_omit=True, poly_deg=0):
     out = np.empty((nt, p))
     rc = lib().orc_direct(kernel, float(eps), poly_deg, int(bool(self_omit)), N, _p(X), _p(W),
                           _p(tg), nt, _p(out))
+    assert rc == 0
+    return out
+
+
+def direct_targets(kernel, eps, X, W, Xt, poly_deg=0):
+    """Direct sum at separate targets Xt (nt x 3) over all sources (no self term)."""
+    m, p = DIMS[kernel]
+    X = _f64(X).reshape(-1, 3)
+    N = X.shape[0]
+    W = _f64(W).reshape(N, m)
+    Xt = _f64(Xt).reshape(-1, 3)
+    out = np.empty((Xt.shape[0], p))
+    rc = lib().orc_direct_targets(kernel, float(eps), poly_deg, N, _p(X), _p(W), _p(Xt), Xt.shape[0], _p(out))
     assert rc == 0
     return out
 

@@ -608,6 +608,44 @@ int orc_treecode(const orc_tree* T, int kernel, double eps, int n, double theta,
     return 0;
 }
 
+/* Treecode velocities at a SEPARATE target set (Algorithm 2 with targets x_i
+ * that need not be sources; "the targets ... may differ from the
+ * sources").  Same traversal as orc_treecode, no self term (no target is a
+ * source); the root and every ancestor of a target's position may be accepted
+ * when the target lies outside them.  xt: nt x 3; out: nt x p; stats optional. */
+int orc_treecode_targets(const orc_tree* T, int kernel, double eps, int n, double theta,
+                         const double* fhat, const double* w, const double* xt, int64_t nt,
+                         double* out, uint64_t* stats)
+{
+    eval_ctx E;
+    memset(&E, 0, sizeof(E));
+    E.T = T;
+    E.K.id = kernel;
+    E.K.eps = eps;
+    E.K.poly_deg = n;
+    if (kernel_dims(kernel, &E.K.m, &E.K.p)) return -1;
+    E.n = n;
+    E.tt = theta * theta;
+    E.self_omit = 0;
+    E.fhat = fhat;
+    int64_t N = T->N;
+    int m = E.K.m, p = E.K.p;
+    double* fs = (double*)malloc((size_t)N * m * sizeof(double));
+    for (int64_t s = 0; s < N; ++s)
+        for (int c = 0; c < m; ++c) fs[s * m + c] = w[T->perm[s] * m + c];
+    E.fs = fs;
+    for (int64_t q = 0; q < nt; ++q) {
+        for (int c = 0; c < 6; ++c) E.acc[c] = 0.0L;
+        memset(E.st, 0, sizeof(E.st));
+        compute_velocity(&E, xt + 3 * q, -1, 0);
+        for (int c = 0; c < p; ++c) out[q * p + c] = (double)E.acc[c];
+        if (stats)
+            for (int c = 0; c < 5; ++c) stats[q * 5 + c] = E.st[c];
+    }
+    free(fs);
+    return 0;
+}
+
 /* ------------------------------------------------------------------------- */
 /* Direct sum and error                                   */
 /* ------------------------------------------------------------------------- */
@@ -627,6 +665,25 @@ int orc_direct(int kernel, double eps, int poly_deg, int self_omit, int64_t N, c
         for (int64_t j = 0; j < N; ++j) {
             if (self_omit && j == i) continue;
             pair_term(&K, xyz + 3 * i, xyz + 3 * j, w + j * K.m, t);
+            for (int c = 0; c < K.p; ++c) acc[c] += t[c];
+        }
+        for (int c = 0; c < K.p; ++c) out[q * K.p + c] = (double)acc[c];
+    }
+    return 0;
+}
+
+/* u(x_q) = sum_j k(x_q, y_j) f_j at separate targets xt (nt x 3), all j
+ * ascending (no self term). */
+int orc_direct_targets(int kernel, double eps, int poly_deg, int64_t N, const double* xyz,
+                       const double* w, const double* xt, int64_t nt, double* out)
+{
+    orc_kernel K = {kernel, 0, 0, eps, poly_deg};
+    if (kernel_dims(kernel, &K.m, &K.p)) return -1;
+    double t[6];
+    for (int64_t q = 0; q < nt; ++q) {
+        long double acc[6] = {0};
+        for (int64_t j = 0; j < N; ++j) {
+            pair_term(&K, xt + 3 * q, xyz + 3 * j, w + j * K.m, t);
             for (int c = 0; c < K.p; ++c) acc[c] += t[c];
         }
         for (int c = 0; c < K.p; ++c) out[q * K.p + c] = (double)acc[c];
