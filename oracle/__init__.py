@@ -56,6 +56,7 @@ def lib():
         L.orc_modified_weights_range.argtypes = [vp, i32, i32, vp, i64, i64, vp]
         L.orc_modified_weights_box.argtypes = [i64, vp, vp, i32, i32, vp, vp, vp]
         L.orc_treecode.argtypes = [vp, i32, d, i32, d, i32, vp, vp, vp, i64, vp, vp]
+        L.orc_treecode_ex.argtypes = [vp, i32, d, i32, d, i32, i32, vp, vp, vp, i64, vp, vp]
         L.orc_direct.argtypes = [i32, d, i32, i32, i64, vp, vp, vp, i64, vp]
         L.orc_treecode_targets.argtypes = [vp, i32, d, i32, d, vp, vp, vp, i64, vp, vp]
         L.orc_direct_targets.argtypes = [i32, d, i32, i64, vp, vp, vp, i64, vp]
@@ -167,7 +168,7 @@ class Tree:
         return F
 
     def treecode(self, kernel, eps, n, theta, W, fhat=None, targets=None, self_omit=True,
-                 stats=False):
+                 stats=False, size_check=False):
         m, p = DIMS[kernel]
         W = _f64(W).reshape(self.N, m)
         if fhat is None:
@@ -176,8 +177,8 @@ class Tree:
         nt = self.N if tg is None else tg.size
         out = np.empty((nt, p))
         st = np.empty((nt, 5), np.uint64) if stats else None
-        rc = lib().orc_treecode(self._h, kernel, float(eps), n, float(theta), int(bool(self_omit)),
-                                _p(_f64(fhat)), _p(W), _p(tg), nt, _p(out), _p(st))
+        rc = lib().orc_treecode_ex(self._h, kernel, float(eps), n, float(theta), int(bool(self_omit)),
+                                   int(bool(size_check)), _p(_f64(fhat)), _p(W), _p(tg), nt, _p(out), _p(st))
         assert rc == 0
         return (out, st) if stats else out
 

@@ -505,6 +505,7 @@ typedef struct {
     int n;
     double tt;        /* theta * theta, RN */
     int self_omit;
+    int size_check;   /* variant: accepted cluster with N_C < (n+1)^3 -> direct */
     const double* fhat;
     const double* fs; /* sorted weights */
     long double acc[6];
@@ -533,7 +534,23 @@ static void compute_velocity(eval_ctx* E, const double* x, int64_t xi_s, int id)
     const orc_node* C = &T->nodes[id];
     int p = E->K.p, m = E->K.m, P = E->n + 1, P3 = P * P * P;
     double t[6];
-    if (mac(C, x, E->tt)) {
+    int accept = mac(C, x, E->tt);
+    if (accept && E->size_check && C->end - C->begin < (int64_t)P3) {
+        /* size-check variant (not in the paper; motivated by its cost argument
+         * "a cost reduction when N_c >> n^3"): an accepted cluster
+         * holding fewer particles than proxies is summed directly over its
+         * particles (Eq. pc_interaction_3D).  The target lies outside an
+         * accepted box (r <= theta R < R), so no self term can occur. */
+        for (int64_t j = C->begin; j < C->end; ++j) {
+            pair_term(&E->K, x, T->xs + 3 * j, E->fs + j * m, t);
+            for (int c = 0; c < p; ++c) E->acc[c] += t[c];
+            E->st[3] += 1;
+        }
+        E->st[2] += 1;
+        E->st[4] += (uint64_t)(C->end - C->begin);
+        return;
+    }
+    if (accept) {
         /* far field, Eq. pc_approximation_3D: target vs the (n+1)^3
          * Chebyshev points s_k with modified weights fhat_k */
         double s[3 * 64], fk[6], y[3];
@@ -572,9 +589,20 @@ static void compute_velocity(eval_ctx* E, const double* x, int64_t xi_s, int id)
 /* Treecode velocities (Algorithm 2 line 7) for the targets `tgt`
  * (ORIGINAL indices; NULL = all N in order), targets = sources.
  * out: nt x p; stats (optional): nt x 5.  w: original order N x m. */
+int orc_treecode_ex(const orc_tree* T, int kernel, double eps, int n, double theta, int self_omit,
+                    int size_check, const double* fhat, const double* w, const int64_t* tgt, int64_t nt,
+                    double* out, uint64_t* stats);
 int orc_treecode(const orc_tree* T, int kernel, double eps, int n, double theta, int self_omit,
                  const double* fhat, const double* w, const int64_t* tgt, int64_t nt,
                  double* out, uint64_t* stats)
+{
+    return orc_treecode_ex(T, kernel, eps, n, theta, self_omit, 0, fhat, w, tgt, nt, out, stats);
+}
+
+/* As orc_treecode, with the size-check variant selectable (size_check != 0). */
+int orc_treecode_ex(const orc_tree* T, int kernel, double eps, int n, double theta, int self_omit,
+                    int size_check, const double* fhat, const double* w, const int64_t* tgt, int64_t nt,
+                    double* out, uint64_t* stats)
 {
     eval_ctx E;
     memset(&E, 0, sizeof(E));
@@ -586,6 +614,7 @@ int orc_treecode(const orc_tree* T, int kernel, double eps, int n, double theta,
     E.n = n;
     E.tt = theta * theta;
     E.self_omit = self_omit;
+    E.size_check = size_check;
     E.fhat = fhat;
     int64_t N = T->N;
     int m = E.K.m, p = E.K.p;
