@@ -121,7 +121,8 @@ def oracle_sample(cfg, X, W, S_targets, weight_frac=0.1, seed=1, fhat=None):
     while cb > 1 and acc < weight_frac * tot:
         cb -= 1
         acc += sizes[cb]
-    F = np.zeros((T.nclusters, 3, (cfg["n"] + 1) ** 3)) if fhat is None else fhat.copy()
+    m = O.DIMS[cfg["kernel"]][0]
+    F = np.zeros((T.nclusters, m, (cfg["n"] + 1) ** 3)) if fhat is None else fhat.copy()
     t0 = time.perf_counter()
     T.modified_weights(W, cfg["n"], cluster_range=(cb, T.nclusters), out=F)
     t_w = (time.perf_counter() - t0) * tot / acc if acc > 0 else 0.0

@@ -146,6 +146,40 @@ kitc_status kitc_eval(const kitc_tree* t, int32_t kernel, int32_t n, double thet
                       double eps, int32_t self, const double* fhat_dev, int64_t batch_begin,
                       int64_t batch_end, double* out_dev, uint64_t* stats_dev, void* s);
 
+/* Treecode at a SEPARATE set of Nt targets (targets need not be
+ * sources): the same traversal, MAC, far field and
+ * near field as kitc_eval, with no self term (every source j is summed), so the
+ * root and the ancestors of a target's position may be accepted when it lies
+ * outside them.  Targets are batched internally along a Morton curve of their
+ * bounding box (scratch owned by the tree handle; one call per handle at a time).
+ *  xt_dev: device double[Nt][3] (any positions; eps = 0 and a target on a
+ *  source gives a non-finite row -- the singular kernel); out_dev: device
+ *  double[Nt][p] in the order of xt_dev; stats_dev optional uint64[Nt][5] as
+ *  kitc_eval.  Other arguments and errors as kitc_eval.  Multi-GPU: each rank
+ *  passes its own slice of the targets. */
+kitc_status kitc_eval_targets(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0,
+                              double eps, const double* fhat_dev, const double* xt_dev, int64_t Nt,
+                              double* out_dev, uint64_t* stats_dev, void* s);
+
+/* Evaluation variants (flags of kitc_eval_ex / kitc_eval_targets_ex). */
+typedef enum {
+    /* Not in the paper, motivated by its cost argument
+     * "a cost reduction when N_c >> n^3": an ACCEPTED cluster with
+     * N_C < (n+1)^3 particles is summed directly over its particles instead of
+     * its (n+1)^3 proxies (counted as a near interaction in stats).  Changes the
+     * result (more exact); the oracle mirrors it (orc_treecode_ex). */
+    KITC_EVAL_SIZE_CHECK = 1
+} kitc_eval_flag;
+
+/* kitc_eval / kitc_eval_targets with variant flags (0 = the paper's method;
+ * unknown bits -> EINVAL). */
+kitc_status kitc_eval_ex(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0, double eps,
+                         int32_t self, uint32_t flags, const double* fhat_dev, int64_t batch_begin,
+                         int64_t batch_end, double* out_dev, uint64_t* stats_dev, void* s);
+kitc_status kitc_eval_targets_ex(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0,
+                                 double eps, uint32_t flags, const double* fhat_dev, const double* xt_dev,
+                                 int64_t Nt, double* out_dev, uint64_t* stats_dev, void* s);
+
 /* Number of targets in batches [0, batch_end) -- for splitting work. */
 kitc_status kitc_batch_targets(const kitc_tree* t, int64_t batch_end, int64_t* n_targets);
 
@@ -156,6 +190,14 @@ kitc_status kitc_batch_targets(const kitc_tree* t, int64_t batch_end, int64_t* n
 kitc_status kitc_direct(int32_t kernel, double eps, int32_t self, const double* x_tgt_dev,
                         int64_t Nt, const double* x_src_dev, const double* w_src_dev, int64_t Ns,
                         double* out_dev, void* s);
+
+/* Direct sum at a SAMPLE of the sources as targets (the paper samples targets
+ * at large N): target q is source idx_dev[q] (device int64[nt],
+ * each in [0, Ns), not checked), self pair j == idx[q] skipped under
+ * KITC_SELF_OMIT.  out_dev double[nt][p].  Other arguments as kitc_direct. */
+kitc_status kitc_direct_sample(int32_t kernel, double eps, int32_t self, const int64_t* idx_dev, int64_t nt,
+                               const double* x_src_dev, const double* w_src_dev, int64_t Ns, double* out_dev,
+                               void* s);
 
 /* Relative error E (Eq. error) of approx vs ref, both device
  * double[count] (rows of p components concatenated).  Writes E to

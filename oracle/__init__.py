@@ -58,7 +58,7 @@ def lib():
         L.orc_treecode.argtypes = [vp, i32, d, i32, d, i32, vp, vp, vp, i64, vp, vp]
         L.orc_treecode_ex.argtypes = [vp, i32, d, i32, d, i32, i32, vp, vp, vp, i64, vp, vp]
         L.orc_direct.argtypes = [i32, d, i32, i32, i64, vp, vp, vp, i64, vp]
-        L.orc_treecode_targets.argtypes = [vp, i32, d, i32, d, vp, vp, vp, i64, vp, vp]
+        L.orc_treecode_targets.argtypes = [vp, i32, d, i32, d, i32, vp, vp, vp, i64, vp, vp]
         L.orc_direct_targets.argtypes = [i32, d, i32, i64, vp, vp, vp, i64, vp]
         L.orc_rel_error.argtypes = [vp, vp, i64, i32]
         L.orc_rel_error.restype = d
@@ -183,7 +183,7 @@ class Tree:
         return (out, st) if stats else out
 
 
-    def treecode_targets(self, kernel, eps, n, theta, W, Xt, fhat=None, stats=False):
+    def treecode_targets(self, kernel, eps, n, theta, W, Xt, fhat=None, stats=False, size_check=False):
         """Treecode at a separate target set Xt (nt x 3); no self term."""
         m, p = DIMS[kernel]
         W = _f64(W).reshape(self.N, m)
@@ -193,7 +193,8 @@ class Tree:
         nt = Xt.shape[0]
         out = np.empty((nt, p))
         st = np.empty((nt, 5), np.uint64) if stats else None
-        rc = lib().orc_treecode_targets(self._h, kernel, float(eps), n, float(theta), _p(_f64(fhat)), _p(W),
+        rc = lib().orc_treecode_targets(self._h, kernel, float(eps), n, float(theta), int(bool(size_check)),
+                                        _p(_f64(fhat)), _p(W),
                                         _p(Xt), nt, _p(out), _p(st))
         assert rc == 0
         return (out, st) if stats else out

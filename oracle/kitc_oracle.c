@@ -641,8 +641,9 @@ int orc_treecode_ex(const orc_tree* T, int kernel, double eps, int n, double the
  * that need not be sources; "the targets ... may differ from the
  * sources").  Same traversal as orc_treecode, no self term (no target is a
  * source); the root and every ancestor of a target's position may be accepted
- * when the target lies outside them.  xt: nt x 3; out: nt x p; stats optional. */
-int orc_treecode_targets(const orc_tree* T, int kernel, double eps, int n, double theta,
+ * when the target lies outside them.  xt: nt x 3; out: nt x p; stats optional;
+ * size_check: the variant of orc_treecode_ex. */
+int orc_treecode_targets(const orc_tree* T, int kernel, double eps, int n, double theta, int size_check,
                          const double* fhat, const double* w, const double* xt, int64_t nt,
                          double* out, uint64_t* stats)
 {
@@ -656,6 +657,7 @@ int orc_treecode_targets(const orc_tree* T, int kernel, double eps, int n, doubl
     E.n = n;
     E.tt = theta * theta;
     E.self_omit = 0;
+    E.size_check = size_check;
     E.fhat = fhat;
     int64_t N = T->N;
     int m = E.K.m, p = E.K.p;

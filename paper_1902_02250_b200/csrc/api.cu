@@ -109,6 +109,29 @@ kitc_status kitc_eval(const kitc_tree* t, int32_t kernel, int32_t n, double thet
     KITC_GUARD(return eval(t, kernel, n, theta, eps, self, fhat, bb, be, out, stats, (cudaStream_t)s);)
 }
 
+kitc_status kitc_eval_ex(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0, double eps,
+                         int32_t self, uint32_t flags, const double* fhat, int64_t bb, int64_t be, double* out,
+                         uint64_t* stats, void* s) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_eval_ex: NULL handle");
+    if (t->built && N0 != t->N0) return set_error(KITC_EINVAL, "kitc_eval_ex: N0 differs from the tree's N0");
+    KITC_GUARD(return eval(t, kernel, n, theta, eps, self, fhat, bb, be, out, stats, (cudaStream_t)s, nullptr,
+                           flags);)
+}
+
+kitc_status kitc_eval_targets(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0, double eps,
+                              const double* fhat, const double* xt, int64_t Nt, double* out, uint64_t* stats,
+                              void* s) {
+    return kitc_eval_targets_ex(t, kernel, n, theta, N0, eps, 0u, fhat, xt, Nt, out, stats, s);
+}
+
+kitc_status kitc_eval_targets_ex(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0,
+                                 double eps, uint32_t flags, const double* fhat, const double* xt, int64_t Nt,
+                                 double* out, uint64_t* stats, void* s) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_eval_targets: NULL handle");
+    if (t->built && N0 != t->N0) return set_error(KITC_EINVAL, "kitc_eval_targets: N0 differs from the tree's N0");
+    KITC_GUARD(return eval_targets(t, kernel, n, theta, eps, fhat, xt, Nt, out, stats, (cudaStream_t)s, flags);)
+}
+
 kitc_status kitc_batch_targets(const kitc_tree* t, int64_t be, int64_t* nt) {
     if (!t || !nt) return set_error(KITC_EINVAL, "kitc_batch_targets: NULL argument");
     if (!t->built) return set_error(KITC_ESTATE, "kitc_batch_targets: tree not built");
@@ -120,6 +143,12 @@ kitc_status kitc_batch_targets(const kitc_tree* t, int64_t be, int64_t* nt) {
 kitc_status kitc_direct(int32_t kernel, double eps, int32_t self, const double* xt, int64_t Nt, const double* xs,
                         const double* ws, int64_t Ns, double* out, void* s) {
     KITC_GUARD(return direct(kernel, eps, self, xt, Nt, xs, ws, Ns, out, (cudaStream_t)s);)
+}
+
+kitc_status kitc_direct_sample(int32_t kernel, double eps, int32_t self, const int64_t* idx, int64_t nt,
+                               const double* xs, const double* ws, int64_t Ns, double* out, void* s) {
+    if (nt > 0 && !idx) return set_error(KITC_EINVAL, "kitc_direct_sample: NULL index array");
+    KITC_GUARD(return direct(kernel, eps, self, xs, nt, xs, ws, Ns, out, (cudaStream_t)s, idx);)
 }
 
 kitc_status kitc_rel_error(const double* ref, const double* ap, int64_t n, double* E, void* s) {

@@ -17,8 +17,11 @@ namespace {
 
 constexpr int kTile = 256;
 
+// tidx (optional): target q is source tidx[q] (sampled targets; its self pair is
+// the one skipped under SELF_OMIT); otherwise target q is xt[q] (self = q).
 template <int KER>
 __global__ void __launch_bounds__(kTile) k_direct(const double* __restrict__ xt, int Nt,
+                                                  const long long* __restrict__ tidx,
                                                   const double* __restrict__ xs,
                                                   const double* __restrict__ ws, int Ns,
                                                   double* __restrict__ out, KParams kp, int self_omit) {
@@ -28,10 +31,12 @@ __global__ void __launch_bounds__(kTile) k_direct(const double* __restrict__ xt,
     const int i = blockIdx.x * kTile + threadIdx.x;
     const bool valid = i < Nt;
     double x = 0, y = 0, z = 0;
+    long long si = i;
     if (valid) {
-        x = xt[3 * (size_t)i];
-        y = xt[3 * (size_t)i + 1];
-        z = xt[3 * (size_t)i + 2];
+        const double* p = tidx ? xs + 3 * (si = tidx[i]) : xt + 3 * (size_t)i;
+        x = p[0];
+        y = p[1];
+        z = p[2];
     }
     double tot[NP];
 #pragma unroll
@@ -56,7 +61,7 @@ __global__ void __launch_bounds__(kTile) k_direct(const double* __restrict__ xt,
 #pragma unroll
             for (int m = 0; m < M; ++m) f[m] = sw[m][jj];
             const double s = fma(dx, dx, fma(dy, dy, fma(dz, dz, kp.e2)));
-            if (!self_omit || tile + jj != i) K::pair(dx, dy, dz, s, f, part, kp);
+            if (!self_omit || tile + jj != si) K::pair(dx, dy, dz, s, f, part, kp);
         }
 #pragma unroll
         for (int c = 0; c < NP; ++c) tot[c] += part[c];
@@ -97,12 +102,13 @@ __global__ void __launch_bounds__(256) k_relerr(const double* __restrict__ ref, 
 }  // namespace
 
 kitc_status direct(int kernel, double eps, int self, const double* xt, int64_t Nt, const double* xs,
-                   const double* ws, int64_t Ns, double* out, cudaStream_t s) {
+                   const double* ws, int64_t Ns, double* out, cudaStream_t s, const int64_t* tidx) {
     if (Nt < 0 || Ns < 0 || Nt > 0x7fffffffLL || Ns > 0x7fffffffLL)
         return set_error(KITC_EINVAL, "kitc_direct: size out of range");
     if (!(eps >= 0.0) || !std::isfinite(eps)) return set_error(KITC_EINVAL, "kitc_direct: eps must be >= 0");
     if (self != KITC_SELF_OMIT && self != KITC_SELF_INCLUDE) return set_error(KITC_EINVAL, "kitc_direct: bad self");
-    if (self == KITC_SELF_OMIT && (xt != xs || Nt != Ns))
+    if (tidx) xt = xs;  // sampled targets: validated by the caller (indices in [0, Ns))
+    if (self == KITC_SELF_OMIT && !tidx && (xt != xs || Nt != Ns))
         return set_error(KITC_EINVAL, "kitc_direct: KITC_SELF_OMIT needs targets == sources");
     if (eps == 0.0 && self != KITC_SELF_OMIT)
         return set_error(KITC_EINVAL, "kitc_direct: eps = 0 requires KITC_SELF_OMIT");
@@ -112,9 +118,9 @@ kitc_status direct(int kernel, double eps, int self, const double* xt, int64_t N
     const int grid = (int)((Nt + kTile - 1) / kTile);
     const int so = self == KITC_SELF_OMIT;
     switch (kernel) {
-        case KITC_STOKESLET: k_direct<0><<<grid, kTile, 0, s>>>(xt, (int)Nt, xs, ws, (int)Ns, out, kp, so); note_launch(); break;
-        case KITC_ROTLET: k_direct<1><<<grid, kTile, 0, s>>>(xt, (int)Nt, xs, ws, (int)Ns, out, kp, so); note_launch(); break;
-        case KITC_STOKESLET_ROTLET: k_direct<2><<<grid, kTile, 0, s>>>(xt, (int)Nt, xs, ws, (int)Ns, out, kp, so); note_launch(); break;
+        case KITC_STOKESLET: k_direct<0><<<grid, kTile, 0, s>>>(xt, (int)Nt, reinterpret_cast<const long long*>(tidx), xs, ws, (int)Ns, out, kp, so); note_launch(); break;
+        case KITC_ROTLET: k_direct<1><<<grid, kTile, 0, s>>>(xt, (int)Nt, reinterpret_cast<const long long*>(tidx), xs, ws, (int)Ns, out, kp, so); note_launch(); break;
+        case KITC_STOKESLET_ROTLET: k_direct<2><<<grid, kTile, 0, s>>>(xt, (int)Nt, reinterpret_cast<const long long*>(tidx), xs, ws, (int)Ns, out, kp, so); note_launch(); break;
         default: return set_error(KITC_EINVAL, "kitc_direct: unknown kernel");
     }
     KITC_CUDA(cudaGetLastError());

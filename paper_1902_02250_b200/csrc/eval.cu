@@ -42,18 +42,22 @@ static_assert(kSB == 1 || kSB == 2, "kSB");
 static_assert(kGroup == kRows, "k_eval: one fhat row per lane of a target group");
 
 struct EvalArgs {
-    const double* x;
+    const double* x;  // sorted sources (SoA)
     const double* y;
     const double* z;
-    const int* perm;
-    const int* tord;
+    const double* tx;  // targets by position t (= x, y, z when targets = sources)
+    const double* ty;
+    const double* tz;
+    const int* perm;  // output row of target position t
+    const int* tord;  // batch slot -> target position (nullptr: identity)
     const double* w;  // sorted weights, M planes of N
     const double4* cr;
     const int4* topo;
     const double* grid;
     const double* fhat;
-    const int* bstart;
+    const int* bstart;  // nullptr: batch b = positions [kBatch b, kBatch b + kBatch) of nt
     const int* bcount;
+    long long nt;
     double* out;
     unsigned long long* stats;
     long long bb, be;
@@ -62,6 +66,7 @@ struct EvalArgs {
     int stack_cap;
     int warp_smem;  // bytes of shared memory per warp (WarpSmem)
     int self_omit;
+    int size_check;  // KITC_EVAL_SIZE_CHECK
     double tt;  // theta * theta (RN)
     KParams kp;
 };
@@ -144,7 +149,7 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
         const double* B = ws.buf + (k & 1) * kSB * blk;
         mbar_wait(ws.bar + (k & 1), (unsigned)(k >> 1) & 1u);
         const int b0 = st * kSB;  // first block of the stage
-        if (kSB == 2 && b0 + 1 < RF) {
+        if (K::kPairRows && kSB == 2 && b0 + 1 < RF) {
             // two full blocks: rows ra, ra + 1 of block h = grp / 4
             const int h = grp >> 2, j = 2 * (grp & 3);
             const int ra = (b0 + h) * kRows + j;
@@ -194,12 +199,22 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
                     const double dx = x - __ldg(g + k1), dy = y - __ldg(g + P + k2);
                     const double pxye = fma(dy, dy, dx * dx) + kp.e2;
                     typename K::Row r;
-                    for (int k3 = 0; k3 < P; ++k3) {
-                        const double dzk = z - __ldg(g + 2 * P + k3);
-                        double f[M];
+                    if constexpr (PT > 0) {
 #pragma unroll
-                        for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + grp];
-                        K::pair_row(dx, dy, dzk, fma(dzk, dzk, pxye), f, acc, r, kp);
+                        for (int k3 = 0; k3 < PT; ++k3) {
+                            double f[M];
+#pragma unroll
+                            for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + grp];
+                            K::pair_row(dx, dy, dz[k3], fma(dz[k3], dz[k3], pxye), f, acc, r, kp);
+                        }
+                    } else {
+                        for (int k3 = 0; k3 < P; ++k3) {
+                            const double dzk = z - __ldg(g + 2 * P + k3);
+                            double f[M];
+#pragma unroll
+                            for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + grp];
+                            K::pair_row(dx, dy, dzk, fma(dzk, dzk, pxye), f, acc, r, kp);
+                        }
                     }
                     K::row_end(dx, dy, r, acc);
                 } else {  // partial last block: pair by pair
@@ -300,10 +315,17 @@ __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_
     int2* stk = ws.stk;
     const long long b = a.bb + (long long)blockIdx.x * kWarps + wl;
     if (b >= a.be) return;  // whole warp
-    const int p0 = a.bstart[b], tc = a.bcount[b];
+    int p0, tc;
+    if (a.bstart) {
+        p0 = a.bstart[b];
+        tc = a.bcount[b];
+    } else {
+        p0 = (int)(b * kBatch);
+        tc = (int)min((long long)kBatch, a.nt - p0);
+    }
     const bool valid = ti < tc;
-    const int t = a.tord[p0 + (valid ? ti : 0)];
-    const double x = a.x[t], y = a.y[t], z = a.z[t];
+    const int t = a.tord ? a.tord[p0 + (valid ? ti : 0)] : p0 + (valid ? ti : 0);
+    const double x = a.tx[t], y = a.ty[t], z = a.tz[t];
     const int P = PT > 0 ? PT : a.P;
     const int P3 = P * P * P;
     const long long LEN = (long long)((P * P + kRows - 1) / kRows) * P * M * kRows;  // fhat doubles per cluster
@@ -332,7 +354,18 @@ __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_
         const unsigned am = __ballot_sync(0xffffffffu, ok);
         const unsigned rm = mask & ~am;
         const int4 tp = a.topo[c];
-        if (am && ok) {
+        if (am && a.size_check && tp.y - tp.x < P3) {
+            // size-check variant (flag KITC_EVAL_SIZE_CHECK): an accepted cluster with
+            // fewer particles than proxies is summed directly (the target is outside it)
+            if (ok) {
+                near_field<KER>(x, y, z, t, tp.x, tp.y, grp, a, acc);
+                if (STATS) {
+                    st[2] += 1;
+                    st[3] += (unsigned long long)(tp.y - tp.x);
+                    st[4] += (unsigned long long)(tp.y - tp.x);
+                }
+            }
+        } else if (am && ok) {
             far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * LEN, acc, a.kp, P, grp,
                                lane, am, ws);
             if (STATS) {
@@ -408,16 +441,19 @@ static void dispatch(int P, const EvalArgs& a, int grid, size_t smem, cudaStream
 }  // namespace
 
 kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps, int self, const double* fhat,
-                 int64_t bb, int64_t be, double* out, uint64_t* stats, cudaStream_t s) {
+                 int64_t bb, int64_t be, double* out, uint64_t* stats, cudaStream_t s, const TargetSet* ts,
+                 unsigned flags) {
+    if (flags & ~(unsigned)KITC_EVAL_SIZE_CHECK) return set_error(KITC_EINVAL, "kitc_eval: unknown flags");
     if (!t->built) return set_error(KITC_ESTATE, "kitc_eval: tree not built");
     if (!t->weights_ready || t->grid_n != n || t->weights_kernel != kernel)
         return set_error(KITC_ESTATE, "kitc_eval: call kitc_modified_weights with the same kernel and n first");
     if (!(theta >= 0.0 && theta < 1.0)) return set_error(KITC_EINVAL, "kitc_eval: theta must be in [0, 1)");
     if (!(eps >= 0.0) || !std::isfinite(eps)) return set_error(KITC_EINVAL, "kitc_eval: eps must be >= 0");
     if (self != KITC_SELF_OMIT && self != KITC_SELF_INCLUDE) return set_error(KITC_EINVAL, "kitc_eval: bad self");
-    if (eps == 0.0 && self != KITC_SELF_OMIT)
+    if (eps == 0.0 && self != KITC_SELF_OMIT && !ts)
         return set_error(KITC_EINVAL, "kitc_eval: eps = 0 requires KITC_SELF_OMIT (singular kernel)");
-    if (bb < 0 || be > t->nbatches || bb > be) return set_error(KITC_EINVAL, "kitc_eval: bad batch range");
+    const int64_t nbatch = ts ? (ts->n + kBatch - 1) / kBatch : t->nbatches;
+    if (bb < 0 || be > nbatch || bb > be) return set_error(KITC_EINVAL, "kitc_eval: bad batch range");
     if (!fhat || !out) return set_error(KITC_EINVAL, "kitc_eval: NULL buffer");
     if (be == bb) return KITC_OK;
     EvalArgs a;
@@ -426,6 +462,9 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     a.z = t->z.as<double>();
     a.perm = t->perm.as<int>();
     a.tord = t->tord.as<int>();
+    a.tx = a.x;
+    a.ty = a.y;
+    a.tz = a.z;
     a.w = t->w.as<double>();
     a.cr = t->cr.as<double4>();
     a.topo = t->topo.as<int4>();
@@ -433,6 +472,17 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     a.fhat = fhat;
     a.bstart = t->bstart.as<int>();
     a.bcount = t->bcount.as<int>();
+    a.nt = t->N;
+    if (ts) {  // separate targets: no self term (reading A8 applies to targets = sources only)
+        a.tx = ts->x;
+        a.ty = ts->y;
+        a.tz = ts->z;
+        a.perm = ts->row;
+        a.tord = nullptr;
+        a.bstart = a.bcount = nullptr;
+        a.nt = ts->n;
+        self = KITC_SELF_INCLUDE;
+    }
     a.out = out;
     a.stats = reinterpret_cast<unsigned long long*>(stats);
     a.bb = bb;
@@ -441,6 +491,7 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     a.P = n + 1;
     a.stack_cap = 8 * (t->depth + 1);
     a.self_omit = self == KITC_SELF_OMIT;
+    a.size_check = (flags & KITC_EVAL_SIZE_CHECK) != 0;
     a.tt = theta * theta;
     a.kp = make_kparams(eps);
     int m = 0;

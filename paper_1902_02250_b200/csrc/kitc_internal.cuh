@@ -97,6 +97,9 @@ struct kitc_tree {
     kitc::HostBuf h_stage, h_cnt;
     // weights scratch
     kitc::DevBuf d_witems, d_wpart;
+    // separate-target scratch (kitc_eval_targets): Morton keys / indices (double
+    // buffers for the radix sort), sorted coordinates, cub temp, bounding box
+    mutable kitc::DevBuf d_tkey, d_tkey2, d_tidx, d_tidx2, d_txyz, d_tcub, d_tbox;
 };
 
 namespace kitc {
@@ -106,12 +109,25 @@ kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N, int32_t N0, c
 kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, int64_t cb,
                              int64_t ce, double* fhat, cudaStream_t s);
 // eval.cu
+// A separate target set, Morton-sorted (targets.cu): coordinates SoA by sorted
+// position, the original row of each, count.  Batches are kBatch consecutive
+// sorted targets.
+struct TargetSet {
+    const double *x, *y, *z;
+    const int* row;
+    int64_t n;
+};
 kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps, int self,
                  const double* fhat, int64_t bb, int64_t be, double* out, uint64_t* stats,
-                 cudaStream_t s);
+                 cudaStream_t s, const TargetSet* ts = nullptr, unsigned flags = 0);
+// targets.cu
+kitc_status eval_targets(const kitc_tree* t, int kernel, int n, double theta, double eps,
+                         const double* fhat, const double* xt, int64_t Nt, double* out,
+                         uint64_t* stats, cudaStream_t s, unsigned flags = 0);
 // direct.cu
 kitc_status direct(int kernel, double eps, int self, const double* xt, int64_t Nt,
-                   const double* xs, const double* ws, int64_t Ns, double* out, cudaStream_t s);
+                   const double* xs, const double* ws, int64_t Ns, double* out, cudaStream_t s,
+                   const int64_t* tidx = nullptr);
 kitc_status rel_error(const double* ref, const double* approx, int64_t count, double* E,
                       cudaStream_t s);
 }  // namespace kitc

@@ -254,6 +254,7 @@ inline KParams make_kparams(double eps) {
 template <int KER> struct EvalKern {
     using K = Kern<KER>;
     static constexpr int M = K::M, P = K::P, NA = K::P;
+    static constexpr bool kPairRows = true;  // far field: two rows per lane (register budget permitting)
     using Row = typename K::Row;
     static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s, const double* f,
                                                 double* acc, const KParams& k) {
@@ -276,6 +277,7 @@ template <int KER> struct EvalKern {
 // 16 FP64 instructions per far-field pair (row form) + the MUFU seed.
 template <> struct EvalKern<0> {
     static constexpr int M = 3, P = 3, NA = 6;
+    static constexpr bool kPairRows = true;
     static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s, const double* f,
                                                 double* acc, const KParams& k) {
         const double Y = rsqrt2_newton(s);
@@ -323,6 +325,7 @@ template <> struct EvalKern<0> {
 // 26 FP64 instructions per far-field pair (row form) + the MUFU seed.
 template <> struct EvalKern<1> {
     static constexpr int M = 3, P = 6, NA = 9;
+    static constexpr bool kPairRows = true;
     static __device__ __forceinline__ void powers(double s, const KParams& k, double& q, double& d1, double& d2) {
         const double Y = rsqrt2_newton(s);
         const double Y2 = Y * Y;
@@ -384,6 +387,96 @@ template <> struct EvalKern<1> {
     static __device__ __forceinline__ double out(const double* acc, int c) {
         return c < 3 ? acc[c] * (1.0 / (64.0 * 3.14159265358979323846))
                      : fma(0.75, acc[c + 3], acc[c]) * (1.0 / (128.0 * 3.14159265358979323846));
+    }
+};
+
+// Stokeslet + rotlet (weights f, n; m = 6, p = 6) with Y = 2 s^{-1/2} and
+// q, d1, d2 as EvalKern<1>, h = Y + (eps^2/4) Y^3 as EvalKern<0>:
+//   16 pi u  = sum f h                      [acc 0..2]
+//            + 1/4 sum [(f.d) d Y^3 + (n x d) q]   [acc 3..5]
+//   128 pi w = sum [n d1 + 2 (f x d) q + 3/4 (n.d) d d2]   [acc 6..8]
+// Far field in row form with single rows per lane (14 row sums).
+template <> struct EvalKern<2> {
+    static constexpr int M = 6, P = 6, NA = 9;
+    static constexpr bool kPairRows = false;
+    static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s, const double* f,
+                                                double* acc, const KParams& k) {
+        const double Y = rsqrt2_newton(s);
+        const double Y2 = Y * Y;
+        const double Y3 = Y2 * Y;
+        const double Y5 = Y3 * Y2;
+        const double Y7 = Y5 * Y2;
+        const double q = fma(k.e2x3_8, Y5, Y3);
+        const double d1 = fma(k.e4x15_32, Y7, -q);
+        const double d2 = fma(k.e2x5_8, Y7, Y5);
+        const double h = fma(k.e2q, Y3, Y);
+        const double* n = f + 3;
+        const double c = fma(f[0], dx, fma(f[1], dy, f[2] * dz)) * Y3;
+        acc[0] = fma(f[0], h, acc[0]);
+        acc[1] = fma(f[1], h, acc[1]);
+        acc[2] = fma(f[2], h, acc[2]);
+        acc[3] = fma(n[1] * dz - n[2] * dy, q, fma(c, dx, acc[3]));
+        acc[4] = fma(n[2] * dx - n[0] * dz, q, fma(c, dy, acc[4]));
+        acc[5] = fma(n[0] * dy - n[1] * dx, q, fma(c, dz, acc[5]));
+        const double q2 = 2.0 * q;
+        const double gd = fma(n[0], dx, fma(n[1], dy, n[2] * dz)) * (0.75 * d2);
+        acc[6] = fma(f[1] * dz - f[2] * dy, q2, fma(gd, dx, fma(n[0], d1, acc[6])));
+        acc[7] = fma(f[2] * dx - f[0] * dz, q2, fma(gd, dy, fma(n[1], d1, acc[7])));
+        acc[8] = fma(f[0] * dy - f[1] * dx, q2, fma(gd, dz, fma(n[2], d1, acc[8])));
+    }
+    struct Row {
+        double C = 0.0, Z = 0.0;                                      // (f.d) Y^3
+        double An0 = 0.0, An1 = 0.0, An2 = 0.0, Bn0 = 0.0, Bn1 = 0.0;  // q n, q dz n
+        double Af0 = 0.0, Af1 = 0.0, Af2 = 0.0, Bf0 = 0.0, Bf1 = 0.0;  // q f, q dz f
+        double T = 0.0, TZ = 0.0;                                     // (n.d) d2
+    };
+    static __device__ __forceinline__ void pair_row(double dx, double dy, double dz, double s, const double* f,
+                                                    double* acc, Row& r, const KParams& k) {
+        const double Y = rsqrt2_newton(s);
+        const double Y2 = Y * Y;
+        const double Y3 = Y2 * Y;
+        const double Y5 = Y3 * Y2;
+        const double Y7 = Y5 * Y2;
+        const double q = fma(k.e2x3_8, Y5, Y3);
+        const double d1 = fma(k.e4x15_32, Y7, -q);
+        const double d2 = fma(k.e2x5_8, Y7, Y5);
+        const double h = fma(k.e2q, Y3, Y);
+        const double* n = f + 3;
+        acc[0] = fma(f[0], h, acc[0]);
+        acc[1] = fma(f[1], h, acc[1]);
+        acc[2] = fma(f[2], h, acc[2]);
+        acc[6] = fma(n[0], d1, acc[6]);
+        acc[7] = fma(n[1], d1, acc[7]);
+        acc[8] = fma(n[2], d1, acc[8]);
+        const double c = fma(f[0], dx, fma(f[1], dy, f[2] * dz)) * Y3;
+        r.C += c;
+        r.Z = fma(c, dz, r.Z);
+        const double qz = q * dz;
+        r.An0 = fma(q, n[0], r.An0);
+        r.An1 = fma(q, n[1], r.An1);
+        r.An2 = fma(q, n[2], r.An2);
+        r.Bn0 = fma(qz, n[0], r.Bn0);
+        r.Bn1 = fma(qz, n[1], r.Bn1);
+        r.Af0 = fma(q, f[0], r.Af0);
+        r.Af1 = fma(q, f[1], r.Af1);
+        r.Af2 = fma(q, f[2], r.Af2);
+        r.Bf0 = fma(qz, f[0], r.Bf0);
+        r.Bf1 = fma(qz, f[1], r.Bf1);
+        const double t = fma(n[0], dx, fma(n[1], dy, n[2] * dz)) * d2;
+        r.T += t;
+        r.TZ = fma(t, dz, r.TZ);
+    }
+    static __device__ __forceinline__ void row_end(double dx, double dy, const Row& r, double* acc) {
+        acc[3] += fma(r.C, dx, fma(-dy, r.An2, r.Bn1));
+        acc[4] += fma(r.C, dy, fma(dx, r.An2, -r.Bn0));
+        acc[5] += r.Z + fma(dy, r.An0, -dx * r.An1);
+        acc[6] += fma(2.0, fma(-dy, r.Af2, r.Bf1), 0.75 * dx * r.T);
+        acc[7] += fma(2.0, fma(dx, r.Af2, -r.Bf0), 0.75 * dy * r.T);
+        acc[8] += fma(2.0, fma(dy, r.Af0, -dx * r.Af1), 0.75 * r.TZ);
+    }
+    static __device__ __forceinline__ double out(const double* acc, int c) {
+        return c < 3 ? fma(0.25, acc[c + 3], acc[c]) * (1.0 / (16.0 * 3.14159265358979323846))
+                     : acc[c + 3] * (1.0 / (128.0 * 3.14159265358979323846));
     }
 };
 

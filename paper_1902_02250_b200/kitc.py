@@ -24,12 +24,13 @@ LIB_PATH = os.environ.get("KITC_LIB") or os.path.join(_HERE, "libkitc.so")  # ov
 KITC_OK, KITC_EINVAL, KITC_ENOMEM, KITC_ECUDA, KITC_ESTATE = 0, -1, -2, -3, -4
 STOKESLET, ROTLET, STOKESLET_ROTLET = 0, 1, 2
 SELF_OMIT, SELF_INCLUDE = 0, 1
+EVAL_SIZE_CHECK = 1   # kitc_eval_flag (include/kitc.h)
 KERNELS = {"stokeslet": STOKESLET, "rotlet": ROTLET, "stokeslet_rotlet": STOKESLET_ROTLET}
 
 # every symbol include/kitc.h declares
 EXPORTS = ("kitc_kernel_dims", "kitc_fhat_cluster_len", "kitc_tree_create", "kitc_build_tree", "kitc_tree_info",
-           "kitc_tree_export", "kitc_modified_weights", "kitc_eval", "kitc_batch_targets",
-           "kitc_direct", "kitc_rel_error", "kitc_tree_free", "kitc_last_error",
+           "kitc_tree_export", "kitc_modified_weights", "kitc_eval", "kitc_eval_ex", "kitc_eval_targets", "kitc_eval_targets_ex", "kitc_batch_targets",
+           "kitc_direct", "kitc_direct_sample", "kitc_rel_error", "kitc_tree_free", "kitc_last_error",
            "kitc_launch_count")
 
 
@@ -143,6 +144,23 @@ def kitc_eval(t, kernel, n, theta, N0, eps, self_mode, fhat_ptr, batch_begin, ba
                  stream_ptr)
 
 
+def kitc_eval_ex(t, kernel, n, theta, N0, eps, self_mode, flags, fhat_ptr, batch_begin, batch_end, out_ptr,
+                 stats_ptr, stream_ptr):
+    return _call("kitc_eval_ex", t, int(kernel), int(n), float(theta), int(N0), float(eps), int(self_mode),
+                 C.c_uint32(int(flags)), fhat_ptr, int(batch_begin), int(batch_end), out_ptr, stats_ptr, stream_ptr)
+
+
+def kitc_eval_targets(t, kernel, n, theta, N0, eps, fhat_ptr, xt_ptr, Nt, out_ptr, stats_ptr, stream_ptr):
+    return _call("kitc_eval_targets", t, int(kernel), int(n), float(theta), int(N0), float(eps), fhat_ptr,
+                 xt_ptr, int(Nt), out_ptr, stats_ptr, stream_ptr)
+
+
+def kitc_eval_targets_ex(t, kernel, n, theta, N0, eps, flags, fhat_ptr, xt_ptr, Nt, out_ptr, stats_ptr,
+                         stream_ptr):
+    return _call("kitc_eval_targets_ex", t, int(kernel), int(n), float(theta), int(N0), float(eps),
+                 C.c_uint32(int(flags)), fhat_ptr, xt_ptr, int(Nt), out_ptr, stats_ptr, stream_ptr)
+
+
 def kitc_batch_targets(t, batch_end):
     v = C.c_int64()
     _call("kitc_batch_targets", t, int(batch_end), C.byref(v))
@@ -202,15 +220,26 @@ class Tree:
         return fhat
 
     def eval(self, kernel, n, theta, eps, fhat, out=None, batch_range=None, self_omit=True,
-             stats=False, stream=None):
+             stats=False, stream=None, size_check=False):
         _, p = kitc_kernel_dims(kernel)
         dev = fhat.device
         if out is None:
             out = torch.zeros((self.N, p), dtype=torch.float64, device=dev)
         st = torch.zeros((self.N, 5), dtype=torch.int64, device=dev) if stats else None
         bb, be = batch_range if batch_range is not None else (0, self.nbatches)
-        kitc_eval(self._h, kernel, n, theta, self.N0, eps, SELF_OMIT if self_omit else SELF_INCLUDE,
-                  _ptr(fhat), bb, be, _ptr(out), _ptr(st), _stream(stream))
+        kitc_eval_ex(self._h, kernel, n, theta, self.N0, eps, SELF_OMIT if self_omit else SELF_INCLUDE,
+                     EVAL_SIZE_CHECK if size_check else 0, _ptr(fhat), bb, be, _ptr(out), _ptr(st), _stream(stream))
+        return (out, st) if stats else out
+
+    def eval_targets(self, kernel, n, theta, eps, fhat, Xt, out=None, stats=False, stream=None, size_check=False):
+        """Treecode at a separate target set Xt[Nt, 3] (device fp64); no self term."""
+        _, p = kitc_kernel_dims(kernel)
+        Xt = _dev_f64(Xt, 3)
+        if out is None:
+            out = torch.zeros((Xt.shape[0], p), dtype=torch.float64, device=Xt.device)
+        st = torch.zeros((Xt.shape[0], 5), dtype=torch.int64, device=Xt.device) if stats else None
+        kitc_eval_targets_ex(self._h, kernel, n, theta, self.N0, eps, EVAL_SIZE_CHECK if size_check else 0,
+                             _ptr(fhat), _ptr(Xt), Xt.shape[0], _ptr(out), _ptr(st), _stream(stream))
         return (out, st) if stats else out
 
     def batch_targets(self, batch_end):
@@ -260,6 +289,18 @@ def direct(X, W, kernel, eps, self_omit=True, targets=None, out=None, stream=Non
         out = torch.empty((T.shape[0], p), dtype=torch.float64, device=X.device)
     kitc_direct(kernel, eps, SELF_OMIT if self_omit else SELF_INCLUDE, _ptr(T), T.shape[0], _ptr(X),
                 _ptr(W), X.shape[0], _ptr(out), _stream(stream))
+    return out
+
+
+def direct_sample(X, W, kernel, eps, idx, self_omit=True, out=None, stream=None):
+    """Direct sum at the sampled targets X[idx] (idx: device int64) over all sources."""
+    m, p = kitc_kernel_dims(kernel)
+    X, W = _dev_f64(X, 3), _dev_f64(W, m)
+    idx = idx.to(device=X.device, dtype=torch.int64).contiguous()
+    if out is None:
+        out = torch.empty((idx.numel(), p), dtype=torch.float64, device=X.device)
+    _call("kitc_direct_sample", int(kernel), float(eps), SELF_OMIT if self_omit else SELF_INCLUDE, _ptr(idx),
+          idx.numel(), _ptr(X), _ptr(W), X.shape[0], _ptr(out), _stream(stream))
     return out
 
 

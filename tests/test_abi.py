@@ -87,3 +87,20 @@ def test_fhat_cluster_len(lib):
     assert lib.kitc_fhat_cluster_len(0, 0, C.byref(ln)) == -1
     assert lib.kitc_fhat_cluster_len(0, 17, C.byref(ln)) == -1
     assert lib.kitc_fhat_cluster_len(7, 4, C.byref(ln)) == -1
+
+
+def test_rods_generator_matches_paper_example2():
+    # N = N_r (M + 1); slab ~16^2 x 9 at N_r = 15^2, ~85^2 x 9 at 80^2
+    import numpy as np
+    import kitc_inputs as KI
+    X, W = KI.particles(15 * 15 * 151, "rods", m=6)
+    assert X.shape == (33975, 3) and W.shape == (33975, 6)       # the paper's smallest N
+    ext = X.max(0) - X.min(0)
+    assert abs(ext[0] - 16) < 1 and abs(ext[1] - 16) < 1 and ext[2] == 9.0
+    X, _ = KI.config_particles("X2")
+    assert X.shape[0] == 966400                                   # Table 5's N
+    ext = X.max(0) - X.min(0)
+    assert abs(ext[0] - 85) < 1 and ext[2] == 9.0
+    # rod 0 follows (x0 + 0.3 cos 2z, y0 + 0.3 sin 2z, z)
+    z = X[:151, 2]
+    assert np.allclose(X[:151, 0] - X[0, 0], 0.3 * (np.cos(2 * z) - 1), atol=1e-12)

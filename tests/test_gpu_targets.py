@@ -1,0 +1,123 @@
+"""GPU parity of the separate-target evaluation (kitc_eval_targets; SURVEY.md
+§8(f) row f2) against the oracle's treecode_targets / direct_targets
+(tests/test_oracle_targets.py pins them).  Gates as the main parity tests:
+treecode <= 1e-10, direct <= 1e-12, interaction counts equal (integers)."""
+import numpy as np
+import pytest
+
+import kitc_inputs as KI
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TREE_GATE = 1e-10
+DIRECT_GATE = 1e-12
+
+
+@pytest.fixture(scope="module")
+def K():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1902_02250_b200 import kitc
+    return kitc
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def targets(nt, seed, spread=1.5):
+    return np.random.default_rng(seed).uniform(-spread, spread, (nt, 3))
+
+
+@pytest.mark.parametrize("N,N0,n,theta,kern,eps,geom,nt,spread", [
+    (8000, 200, 8, 0.7, 0, 0.01, "uniform", 3001, 1.5),    # inside and outside the source box
+    (6000, 100, 5, 0.6, 1, 0.02, "uniform", 2000, 3.0),    # rotlet, many exterior targets
+    (5000, 150, 4, 0.7, 2, 0.05, "sphere", 1999, 1.2),     # Stokeslet + rotlet, surface sources
+    (3000, 40, 12, 0.7, 0, 0.01, "uniform", 777, 1.0),     # generic (runtime-P) kernel
+    (2000, 50, 3, 0.0, 0, 0.01, "uniform", 500, 1.0),      # theta = 0 -> direct
+    (1000, 30, 6, 0.7, 0, 0.01, "uniform", 5, 50.0),       # ragged batch, far: root accepted
+    (1000, 30, 6, 0.7, 0, 0.01, "uniform", 1, 0.5),        # one target
+])
+def test_eval_targets_parity(K, N, N0, n, theta, kern, eps, geom, nt, spread):
+    m = O.DIMS[kern][0]
+    X, W = KI.particles(N, geom, seed=13, m=m)
+    Xt = targets(nt, 14, spread)
+    T = O.Tree(X, N0)
+    ref, rst = T.treecode_targets(kern, eps, n, theta, W, Xt, stats=True)
+    G = K.Tree(dev(X), N0)
+    fh = G.modified_weights(kern, n, dev(W))
+    got, gst = G.eval_targets(kern, n, theta, eps, fh, dev(Xt), stats=True)
+    assert O.rel_error(ref, host(got)) <= TREE_GATE
+    assert np.array_equal(rst.astype(np.int64), host(gst))
+
+
+def test_eval_targets_equals_self_include_on_sources(K):
+    # targets = sources: per-target results do not depend on the batching -> bitwise equal
+    X, W = KI.particles(20000, seed=3)
+    G = K.Tree(dev(X), 300)
+    fh = G.modified_weights(0, 7, dev(W))
+    a = G.eval(0, 7, 0.7, 0.01, fh, self_omit=False)
+    b = G.eval_targets(0, 7, 0.7, 0.01, fh, dev(X))
+    assert torch.equal(a, b)
+
+
+def test_eval_targets_empty_and_errors(K):
+    X, W = KI.particles(500, seed=1)
+    G = K.Tree(dev(X), 50)
+    fh = G.modified_weights(0, 4, dev(W))
+    out = G.eval_targets(0, 4, 0.7, 0.01, fh, torch.zeros((0, 3), dtype=torch.float64, device="cuda"))
+    assert out.shape == (0, 3)
+    with pytest.raises(K.KitcError):
+        G.eval_targets(0, 5, 0.7, 0.01, fh, dev(targets(10, 0)))     # n mismatch
+    with pytest.raises(K.KitcError):
+        G.eval_targets(0, 4, 1.0, 0.01, fh, dev(targets(10, 0)))     # theta >= 1
+
+
+@pytest.mark.parametrize("kern", [0, 1, 2])
+def test_direct_targets_parity(K, kern):
+    m = O.DIMS[kern][0]
+    X, W = KI.particles(3001, seed=17, m=m)
+    Xt = targets(999, 18)
+    ref = O.direct_targets(kern, 0.01, X, W, Xt)
+    got = host(K.direct(dev(X), dev(W), kern, 0.01, self_omit=False, targets=dev(Xt)))
+    assert O.rel_error(ref, got) <= DIRECT_GATE
+
+
+@pytest.mark.parametrize("kern,self_omit", [(0, True), (1, True), (2, False)])
+def test_direct_sample_parity(K, kern, self_omit):
+    # sampled targets: the oracle's targets= subset with the self term by index
+    m = O.DIMS[kern][0]
+    X, W = KI.particles(5003, seed=19, m=m)
+    tg = KI.sample_targets(5003, 301, seed=2)
+    ref = O.direct(kern, 0.01, X, W, targets=tg, self_omit=self_omit)
+    got = host(K.direct_sample(dev(X), dev(W), kern, 0.01, torch.from_numpy(tg).cuda(), self_omit=self_omit))
+    assert O.rel_error(ref, got) <= DIRECT_GATE
+    full = host(K.direct(dev(X), dev(W), kern, 0.01, self_omit=self_omit))
+    assert np.array_equal(full[tg], got)          # same per-target arithmetic as the full sum
+
+
+@pytest.mark.parametrize("N,N0,n,kern", [(20000, 500, 8, 0), (8000, 60, 4, 1), (3000, 10, 6, 2)])
+def test_size_check_parity(K, N, N0, n, kern):
+    # variant f4: accepted clusters with N_C < (n+1)^3 summed directly (oracle mirrors it)
+    m = O.DIMS[kern][0]
+    X, W = KI.particles(N, seed=29, m=m)
+    T = O.Tree(X, N0)
+    ref, rst = T.treecode(kern, 0.01, n, 0.7, W, stats=True, size_check=True)
+    G = K.Tree(dev(X), N0)
+    fh = G.modified_weights(kern, n, dev(W))
+    got, gst = G.eval(kern, n, 0.7, 0.01, fh, stats=True, size_check=True)
+    assert O.rel_error(ref, host(got)) <= TREE_GATE
+    assert np.array_equal(rst.astype(np.int64), host(gst))
+    # separate targets with the variant
+    Xt = targets(999, 30)
+    ref_t, rst_t = T.treecode_targets(kern, 0.01, n, 0.7, W, Xt, stats=True, size_check=True)
+    got_t, gst_t = G.eval_targets(kern, n, 0.7, 0.01, fh, dev(Xt), stats=True, size_check=True)
+    assert O.rel_error(ref_t, host(got_t)) <= TREE_GATE
+    assert np.array_equal(rst_t.astype(np.int64), host(gst_t))

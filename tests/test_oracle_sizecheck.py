@@ -67,3 +67,12 @@ def test_interaction_lists_brute_force_size_check(N, N0, n):
         assert list(st[i]) == [len(far), len(far) * P3, len(direct), sum(sz[c] for c in direct) - 1, covered]
         nsmall += len(small)
     assert nsmall > 0
+
+
+def test_targets_all_small_equals_direct():
+    X, W = KI.particles(300, seed=3)
+    Xt = np.random.default_rng(9).uniform(-2, 2, (80, 3))
+    T = O.Tree(X, 10)
+    u, st = T.treecode_targets(O.STOKESLET, 0.01, 6, 0.7, W, Xt, stats=True, size_check=True)
+    assert st[:, 0].sum() == 0
+    assert O.rel_error(O.direct_targets(O.STOKESLET, 0.01, X, W, Xt), u) < 1e-13
