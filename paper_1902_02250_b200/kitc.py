@@ -53,14 +53,21 @@ def _load():
         "kitc_tree_info": [vp, P(i64), P(i32), P(i64), P(i32)],
         "kitc_tree_export": [vp] + [vp] * 9,
         "kitc_modified_weights": [vp, i32, i32, vp, i64, i64, vp, vp],
+        "kitc_fhat_cluster_len": [i32, i32, P(i64)],
         "kitc_eval": [vp, i32, i32, d, i32, d, i32, vp, i64, i64, vp, vp, vp],
+        "kitc_eval_ex": [vp, i32, i32, d, i32, d, i32, C.c_uint32, vp, i64, i64, vp, vp, vp],
+        "kitc_eval_targets": [vp, i32, i32, d, i32, d, vp, vp, i64, vp, vp, vp],
+        "kitc_eval_targets_ex": [vp, i32, i32, d, i32, d, C.c_uint32, vp, vp, i64, vp, vp, vp],
         "kitc_batch_targets": [vp, i64, P(i64)],
         "kitc_direct": [i32, d, i32, vp, i64, vp, vp, i64, vp, vp],
+        "kitc_direct_sample": [i32, d, i32, vp, i64, vp, vp, i64, vp, vp],
         "kitc_rel_error": [vp, vp, i64, P(d), vp],
         "kitc_tree_free": [vp],
         "kitc_last_error": [],
         "kitc_launch_count": [],
     }
+    global SIGNATURES
+    SIGNATURES = sig
     for name, args in sig.items():
         f = getattr(L, name)
         f.argtypes = args

@@ -104,3 +104,15 @@ def test_rods_generator_matches_paper_example2():
     # rod 0 follows (x0 + 0.3 cos 2z, y0 + 0.3 sin 2z, z)
     z = X[:151, 2]
     assert np.allclose(X[:151, 0] - X[0, 0], 0.3 * (np.cos(2 * z) - 1), atol=1e-12)
+
+
+def test_binding_declares_every_signature():
+    # every exported call has ctypes argtypes (no implicit int/float conversion)
+    from paper_1902_02250_b200 import kitc
+    assert sorted(kitc.SIGNATURES) == sorted(kitc.EXPORTS)
+    src = open(os.path.join(ROOT, "include", "kitc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    for name, args in kitc.SIGNATURES.items():
+        m = re.search(r"\b" + name + r"\s*\(([^)]*)\)", src)
+        params = [p for p in m.group(1).split(",") if p.strip() and p.strip() != "void"]
+        assert len(params) == len(args), name
