@@ -146,7 +146,7 @@ kitc_status kitc_eval(const kitc_tree* t, int32_t kernel, int32_t n, double thet
                       double eps, int32_t self, const double* fhat_dev, int64_t batch_begin,
                       int64_t batch_end, double* out_dev, uint64_t* stats_dev, void* s);
 
-/* Treecode at a SEPARATE set of Nt targets (P:733-734: targets need not be
+/* Treecode at a SEPARATE set of Nt targets (P:732-733: targets need not be
  * sources): the same traversal, MAC, far field and
  * near field as kitc_eval, with no self term (every source j is summed), so the
  * root and the ancestors of a target's position may be accepted when it lies

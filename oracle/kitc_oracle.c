@@ -638,8 +638,8 @@ int orc_treecode_ex(const orc_tree* T, int kernel, double eps, int n, double the
 }
 
 /* Treecode velocities at a SEPARATE target set (Algorithm 2 with targets x_i
- * that need not be sources; "the targets ... may differ from the
- * sources").  Same traversal as orc_treecode, no self term (no target is a
+ * that need not be sources; "the targets and sources coincide, but
+ * this is not an essential restriction").  Same traversal as orc_treecode, no self term (no target is a
  * source); the root and every ancestor of a target's position may be accepted
  * when the target lies outside them.  xt: nt x 3; out: nt x p; stats optional;
  * size_check: the variant of orc_treecode_ex. */

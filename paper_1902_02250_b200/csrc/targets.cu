@@ -1,4 +1,4 @@
-// targets.cu -- treecode evaluation at a SEPARATE target set (P:733-734: the
+// targets.cu -- treecode evaluation at a SEPARATE target set (P:732-733: the
 // targets need not be the sources).
 //
 // The targets are ordered along a Morton curve of their own bounding box so

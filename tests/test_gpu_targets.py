@@ -1,5 +1,5 @@
 """GPU parity of the separate-target evaluation (kitc_eval_targets; SURVEY.md
-§8(f) row f2, P:733-734) against the oracle's treecode_targets / direct_targets
+§8(f) row f2, P:732-733) against the oracle's treecode_targets / direct_targets
 (tests/test_oracle_targets.py pins them).  Gates as the main parity tests:
 treecode <= 1e-10, direct <= 1e-12, interaction counts equal (integers)."""
 import numpy as np

@@ -1,5 +1,5 @@
 """Oracle pins for the separate-target evaluation (
-P:733-734: the targets need not be the sources).  Targets are no sources, so no
+P:732-733: the targets need not be the sources).  Targets are no sources, so no
 self term; the root and any ancestor of a target's position can be accepted.
 
 Pins (each against something other than the function itself):
