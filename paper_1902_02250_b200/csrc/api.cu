@@ -1,3 +1,4 @@
+#include <algorithm>
 // api.cu -- the extern "C" entry points of libkitc.so (include/kitc.h).
 // Argument checks + exception barrier; the work is in tree.cu, weights.cu,
 // eval.cu and direct.cu.
@@ -136,7 +137,15 @@ kitc_status kitc_batch_targets(const kitc_tree* t, int64_t be, int64_t* nt) {
     if (!t || !nt) return set_error(KITC_EINVAL, "kitc_batch_targets: NULL argument");
     if (!t->built) return set_error(KITC_ESTATE, "kitc_batch_targets: tree not built");
     if (be < 0 || be > t->nbatches) return set_error(KITC_EINVAL, "kitc_batch_targets: bad batch index");
-    *nt = t->h_bprefix[be];
+    // batches tile the sorted positions leaf by leaf: batch b of leaf l starts at
+    // leaf_begin_l + kBatch (b - boff_l), and that is the number of targets before it
+    const auto& bo = t->h_leaf_boff;
+    if (be == t->nbatches) {
+        *nt = t->N;
+        return KITC_OK;
+    }
+    const size_t l = (size_t)(std::upper_bound(bo.begin(), bo.end() - 1, be) - bo.begin()) - 1;
+    *nt = t->h_leaf_begin[l] + (int64_t)kBatch * (be - bo[l]);
     return KITC_OK;
 }
 
@@ -160,8 +169,10 @@ void kitc_tree_free(kitc_tree* t) {
     cudaStream_t s = t->stream;
     for (DevBuf* b : {&t->x, &t->y, &t->z, &t->perm, &t->x2, &t->y2, &t->z2, &t->perm2, &t->w, &t->box, &t->cr,
                       &t->topo, &t->grid, &t->tord, &t->leaves, &t->bstart, &t->bcount, &t->d_items, &t->d_part, &t->d_cnt, &t->d_off,
-                      &t->d_lvl, &t->d_split, &t->d_flag, &t->d_witems, &t->d_wpart})
+                      &t->d_lvl, &t->d_split, &t->d_flag, &t->d_witems, &t->d_wpart, &t->d_tkey, &t->d_tkey2,
+                      &t->d_tidx, &t->d_tidx2, &t->d_txyz, &t->d_tcub, &t->d_tbox})
         b->release(s);
+    if (t->ev_stage) cudaEventDestroy(t->ev_stage);
     t->h_stage.release();
     t->h_cnt.release();
     delete t;

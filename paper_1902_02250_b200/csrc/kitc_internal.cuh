@@ -83,14 +83,15 @@ struct kitc_tree {
     kitc::DevBuf topo;   // int4[C]       begin, end, first_child, nchild
     kitc::DevBuf grid;   // double[C][3][n+1]
     kitc::DevBuf tord;   // int32[N] targets in Morton order inside each leaf (batching only)
-    kitc::DevBuf leaves; // int4[nleaves] begin, end, cluster id
+    kitc::DevBuf leaves; // int4[nleaves] begin, end, cluster id, first batch
     kitc::DevBuf bstart; // int32[nbatches] first position (in tord) of the batch
     kitc::DevBuf bcount; // int32[nbatches]
 
     // host mirrors of the topology
     std::vector<int32_t> h_begin, h_end, h_level, h_parent, h_first, h_nchild;
-    std::vector<int32_t> h_bstart, h_bcount;
-    std::vector<int64_t> h_bprefix;      // targets in batches [0, b)
+    std::vector<int32_t> h_leaf_begin;   // leaves in range order: first sorted position
+    std::vector<int64_t> h_leaf_boff;    // first batch of each leaf (+ total at the end)
+    cudaEvent_t ev_stage = nullptr;      // last build's staging copies (h_stage reuse)
 
     // build scratch
     kitc::DevBuf d_items, d_part, d_cnt, d_off, d_lvl, d_split, d_flag;

@@ -15,6 +15,10 @@
 #include <cfloat>
 #include <cmath>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "kitc_internal.cuh"
 
 namespace kitc {
@@ -245,10 +249,16 @@ __device__ __forceinline__ unsigned int spread3(unsigned int v) {  // 10 bits ->
 
 __global__ void __launch_bounds__(256) k_leaf_order(const int4* __restrict__ leaves, const double* __restrict__ box,
                                                     const double* __restrict__ x, const double* __restrict__ y,
-                                                    const double* __restrict__ z, int* __restrict__ tord) {
+                                                    const double* __restrict__ z, int* __restrict__ tord,
+                                                    int* __restrict__ bstart, int* __restrict__ bcount) {
     __shared__ unsigned long long key[kSortMax];
     const int4 lf = leaves[blockIdx.x];
     const int b = lf.x, n = lf.y - lf.x, c = lf.z;
+    // the leaf's warp batches: kBatch consecutive positions of its Morton order
+    for (int i = threadIdx.x; i * kBatch < n; i += blockDim.x) {
+        bstart[lf.w + i] = b + i * kBatch;
+        bcount[lf.w + i] = min(kBatch, n - i * kBatch);
+    }
     if (n > kSortMax) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) tord[b + i] = b + i;
         return;
@@ -297,7 +307,26 @@ static size_t pad16(size_t n) {
 
 }  // namespace
 
+// KITC_TRACE=1: host timestamps of the build phases on stderr (latency tuning only)
+static bool trace_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("KITC_TRACE");
+        return e && *e == '1';
+    }();
+    return on;
+}
+static void trace(const char* what, int level) {
+    if (!trace_on()) return;
+    static auto t0 = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    if (level < 0) t0 = now;
+    std::fprintf(stderr, "[kitc build] %8.1f us  %s %d\n",
+                 std::chrono::duration<double, std::micro>(now - t0).count(), what, level);
+}
+
 kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N64, int32_t N0, cudaStream_t s) {
+    trace("start", -1);
+    if (t->ev_stage) KITC_CUDA(cudaEventSynchronize(t->ev_stage));  // previous build's staging copies
     if (N64 < 1 || N64 > 0x7fffffffLL) return set_error(KITC_EINVAL, "kitc_build_tree: N out of range");
     if (N0 < 1) return set_error(KITC_EINVAL, "kitc_build_tree: N0 < 1");
     if (!xyz) return set_error(KITC_EINVAL, "kitc_build_tree: xyz is NULL");
@@ -391,6 +420,7 @@ kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N64, int32_t N0,
             k_part_count<<<npi, kThreads, 0, s>>>(reinterpret_cast<Item*>(ds + o1), x, y, z,
                                                  t->d_split.as<double4>(), t->d_cnt.as<int>()); note_launch();
         KITC_CUDA(cudaGetLastError());
+        trace("enqueued bbox/count", level);
         // read counts (+ the non-finite flag at level 0)
         const size_t cb = (size_t)npi * 8 * sizeof(int);
         KITC_TRY(t->h_cnt.ensure(cb + 16));
@@ -398,6 +428,7 @@ kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N64, int32_t N0,
         if (npi) KITC_CUDA(cudaMemcpyAsync(hc, t->d_cnt.p, cb, cudaMemcpyDeviceToHost, s));
         if (level == 0) KITC_CUDA(cudaMemcpyAsync(hc + npi * 8, t->d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         KITC_CUDA(cudaStreamSynchronize(s));
+        trace("counts on host", level);
         if (level == 0 && hc[npi * 8] != 0)
             return set_error(KITC_EINVAL, "kitc_build_tree: non-finite coordinate");
         // (4) scan: offsets per (item, code); children
@@ -460,8 +491,9 @@ kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N64, int32_t N0,
             k_copy_back<<<nsi, kThreads, 0, s>>>(reinterpret_cast<Item*>(dd), t->x2.as<double>(), t->y2.as<double>(),
                                                  t->z2.as<double>(), t->perm2.as<int>(), x, y, z, perm); note_launch();
             KITC_CUDA(cudaGetLastError());
-            // the staging buffer is rewritten next level only after a stream sync
-            KITC_CUDA(cudaStreamSynchronize(s));
+            trace("enqueued scatter", level);
+            // no sync: the host next writes h_cnt after the next level's count sync, which
+            // (stream order) follows this copy
         }
         if (!next.empty()) depth = level + 1;
         cur.swap(next);
@@ -471,46 +503,45 @@ kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N64, int32_t N0,
     t->nclusters = C;
     t->depth = depth;
     t->ndegenerate = ndeg;
-    // topology table + batches
+    // topology table + batches: leaves in order of their ranges (they tile [0, N)); leaf l owns
+    // batches [boff_l, boff_l + ceil(n_l / kBatch)), written on the device by k_leaf_order
     std::vector<std::pair<int, int>> leaves;
     for (int c = 0; c < C; ++c)
         if (hn[c] == 0) leaves.emplace_back(hb[c], c);
     std::sort(leaves.begin(), leaves.end());
-    t->h_bstart.clear();
-    t->h_bcount.clear();
-    t->h_bprefix.assign(1, 0);
-    for (auto& lf : leaves) {
-        const int c = lf.second;
-        for (int b = hb[c]; b < he[c]; b += kBatch) {
-            const int cnt = std::min(kBatch, he[c] - b);
-            t->h_bstart.push_back(b);
-            t->h_bcount.push_back(cnt);
-            t->h_bprefix.push_back(t->h_bprefix.back() + cnt);
-        }
-    }
-    const int nb = (int)t->h_bstart.size();
     const int nlv = (int)leaves.size();
+    t->h_leaf_begin.resize(nlv);
+    t->h_leaf_boff.resize(nlv + 1);
+    int64_t nb = 0;
+    for (int i = 0; i < nlv; ++i) {
+        const int c = leaves[i].second;
+        t->h_leaf_begin[i] = hb[c];
+        t->h_leaf_boff[i] = nb;
+        nb += (he[c] - hb[c] + kBatch - 1) / kBatch;
+    }
+    t->h_leaf_boff[nlv] = nb;
     t->nbatches = nb;
-    const size_t q1 = pad16<int4>(C), q2 = q1 + pad16<int>(nb), q3 = q2 + pad16<int>(nb), q4 = q3 + pad16<int4>(nlv);
-    KITC_TRY(t->h_stage.ensure(q4));
+    const size_t q1 = pad16<int4>(C), q2 = q1 + pad16<int4>(nlv);
+    KITC_TRY(t->h_stage.ensure(q2));
     int4* ht = t->h_stage.as<int4>();
     for (int c = 0; c < C; ++c) ht[c] = make_int4(hb[c], he[c], hf[c], hn[c]);
-    std::copy(t->h_bstart.begin(), t->h_bstart.end(), reinterpret_cast<int*>(t->h_stage.as<char>() + q1));
-    std::copy(t->h_bcount.begin(), t->h_bcount.end(), reinterpret_cast<int*>(t->h_stage.as<char>() + q2));
-    int4* hlv = reinterpret_cast<int4*>(t->h_stage.as<char>() + q3);
-    for (int i = 0; i < nlv; ++i) hlv[i] = make_int4(hb[leaves[i].second], he[leaves[i].second], leaves[i].second, 0);
+    int4* hlv = reinterpret_cast<int4*>(t->h_stage.as<char>() + q1);
+    for (int i = 0; i < nlv; ++i)
+        hlv[i] = make_int4(hb[leaves[i].second], he[leaves[i].second], leaves[i].second, (int)t->h_leaf_boff[i]);
     KITC_TRY(t->topo.ensure(q1, s));
-    KITC_TRY(t->bstart.ensure(q2 - q1, s));
-    KITC_TRY(t->bcount.ensure(q3 - q2, s));
-    KITC_TRY(t->leaves.ensure(q4 - q3, s));
+    KITC_TRY(t->bstart.ensure((size_t)std::max<int64_t>(nb, 1) * sizeof(int), s));
+    KITC_TRY(t->bcount.ensure((size_t)std::max<int64_t>(nb, 1) * sizeof(int), s));
+    KITC_TRY(t->leaves.ensure(q2 - q1, s));
     KITC_TRY(t->tord.ensure((size_t)N * sizeof(int), s));
     KITC_CUDA(cudaMemcpyAsync(t->topo.p, t->h_stage.p, (size_t)C * sizeof(int4), cudaMemcpyHostToDevice, s));
-    KITC_CUDA(cudaMemcpyAsync(t->bstart.p, t->h_stage.as<char>() + q1, (size_t)nb * sizeof(int), cudaMemcpyHostToDevice, s));
-    KITC_CUDA(cudaMemcpyAsync(t->bcount.p, t->h_stage.as<char>() + q2, (size_t)nb * sizeof(int), cudaMemcpyHostToDevice, s));
     KITC_CUDA(cudaMemcpyAsync(t->leaves.p, hlv, (size_t)nlv * sizeof(int4), cudaMemcpyHostToDevice, s));
-    k_leaf_order<<<nlv, 256, 0, s>>>(t->leaves.as<int4>(), t->box.as<double>(), x, y, z, t->tord.as<int>()); note_launch();
+    k_leaf_order<<<nlv, 256, 0, s>>>(t->leaves.as<int4>(), t->box.as<double>(), x, y, z, t->tord.as<int>(),
+                                      t->bstart.as<int>(), t->bcount.as<int>()); note_launch();
     KITC_CUDA(cudaGetLastError());
-    KITC_CUDA(cudaStreamSynchronize(s));
+    // h_stage may still be read by the copies above: the next writer waits on this event
+    if (!t->ev_stage) KITC_CUDA(cudaEventCreateWithFlags(&t->ev_stage, cudaEventDisableTiming));
+    KITC_CUDA(cudaEventRecord(t->ev_stage, s));
+    trace("enqueued topology", level);
     t->built = true;
     return KITC_OK;
 }

@@ -226,12 +226,15 @@ kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, i
         }
     }
     const size_t o1 = (items.size() * sizeof(WItem) + 15) / 16 * 16, o2 = o1 + red.size() * sizeof(RItem);
-    KITC_CUDA(cudaStreamSynchronize(s));  // staging buffer reuse
+    // staging buffer reuse: wait for the copies that last read h_stage (not the whole stream)
+    if (t->ev_stage) KITC_CUDA(cudaEventSynchronize(t->ev_stage));
     KITC_TRY(t->h_stage.ensure(o2));
     std::copy(items.begin(), items.end(), t->h_stage.as<WItem>());
     std::copy(red.begin(), red.end(), reinterpret_cast<RItem*>(t->h_stage.as<char>() + o1));
     KITC_TRY(t->d_witems.ensure(o2, s));
     KITC_CUDA(cudaMemcpyAsync(t->d_witems.p, t->h_stage.p, o2, cudaMemcpyHostToDevice, s));
+    if (!t->ev_stage) KITC_CUDA(cudaEventCreateWithFlags(&t->ev_stage, cudaEventDisableTiming));
+    KITC_CUDA(cudaEventRecord(t->ev_stage, s));
     KITC_TRY(t->d_wpart.ensure((size_t)std::max(nslots, 1) * LEN * sizeof(double), s));
     const WItem* di = t->d_witems.as<WItem>();
     if (m == 3)
