@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip E vs the GPU direct sum")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 fhat exchange: fused peer-memory stores (default) or NCCL all-gather")
     return ap.parse_args()
 
 
@@ -199,13 +201,34 @@ def run_kitc(args, cfg, rank, world, local_rank):
     shard_base = gathered[rank].data_ptr() - cb * row    # virtual base: cluster c -> shard row c - cb
     import ctypes as Cc
 
+    def weights_nccl():
+        kitc.kitc_modified_weights(T.handle, kern, n, kitc._ptr(Wd), cb, ce, Cc.c_void_p(shard_base),
+                                   kitc._stream())
+        D.all_gather_fhat(fhat, gathered, gathered[rank], cshards, rank)
+
+    exchange = "none (1 GPU)"
+    if world > 1 and args.exchange == "p2p":
+        # fused weights + exchange over peer memory; cross-checked bitwise against the NCCL path
+        pf = D.PeerFhat(C, L, dev)
+        fhat_p2p = pf.modified_weights(T, kern, n, Wd, (cb, ce))
+        weights_nccl()
+        torch.cuda.synchronize()
+        ok = torch.tensor([int(torch.equal(fhat_p2p[1:], fhat[1:]))], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok[0]) != 1:
+            raise RuntimeError("fused peer-memory fhat differs from the NCCL all-gather")
+        fhat = fhat_p2p
+        exchange = f"fused modified weights -> {world} peer replicas (symmetric memory, device barriers)"
+    elif world > 1:
+        exchange = "NCCL all_gather_into_tensor of padded fhat shards"
+
     def weights():
         if world == 1:
             T.modified_weights(kern, n, Wd, cluster_range=(cb, ce), fhat=fhat)
+        elif args.exchange == "p2p":
+            pf.modified_weights(T, kern, n, Wd, (cb, ce))
         else:
-            kitc.kitc_modified_weights(T.handle, kern, n, kitc._ptr(Wd), cb, ce, Cc.c_void_p(shard_base),
-                                       kitc._stream())
-            D.all_gather_fhat(fhat, gathered, gathered[rank], cshards, rank)
+            weights_nccl()
 
     ev_e0, ev_e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
@@ -333,7 +356,8 @@ def run_kitc(args, cfg, rank, world, local_rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (kitc_inputs: {cfg['geometry']}, weights uniform [-1,1]^m, seed 0)",
             "config": {"workload": f"{args.config} ({KI.CONFIGS[args.config]})",
-                       "parallelism": f"tree replicated, fhat sharded + NCCL all-gather, targets dp{world}",
+                       "parallelism": f"tree replicated, fhat sharded, targets dp{world}",
+                       "fhat_exchange": exchange,
                        "l2": "flushed between timed steps (256 MB write, untimed)",
                        "clusters": C, "depth": T.depth, "batches": T.nbatches},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -127,6 +127,20 @@ kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const
                                   int64_t cluster_begin, int64_t cluster_end, double* fhat_dev,
                                   void* s);
 
+/* Fused modified weights + replication for the multi-GPU path (SURVEY.md §8(e),
+ * §8(f) f3): as kitc_modified_weights, but every computed cluster slice is
+ * stored into each of the npeers buffers fhat_peers[0..npeers-1] (host array
+ * of device pointers, npeers in [1, 8], each a full double[C][L] f-hat in the
+ * same layout).  On a node the entries are the peer GPUs' f-hat buffers mapped
+ * into this process (CUDA IPC / symmetric memory over NVLink 5 / NVSwitch), so
+ * when every rank calls this for its own cluster range and then all ranks pass
+ * a barrier, every rank holds the full f-hat -- the all-gather is done by the
+ * kernel's own stores, overlapped with its compute.  The caller provides the
+ * barrier (stream-ordered after this call).  npeers = 1 is kitc_modified_weights. */
+kitc_status kitc_modified_weights_peers(kitc_tree* t, int32_t kernel, int32_t n, const double* w_dev,
+                                        int64_t cluster_begin, int64_t cluster_end,
+                                        double* const* fhat_peers, int32_t npeers, void* s);
+
 /* Treecode evaluation (Algorithm 2 lines 7-17) for the targets of
  * batches [batch_begin, batch_end): per target, depth-first over the tree;
  * MAC accept iff R^2 > 0 and r^2 <= (theta*theta) R^2 (R = distance to the box

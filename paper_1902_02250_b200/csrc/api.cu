@@ -99,7 +99,14 @@ kitc_status kitc_tree_export(const kitc_tree* t, int64_t* perm, int64_t* begin, 
 kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const double* w, int64_t cb,
                                   int64_t ce, double* fhat, void* s) {
     if (!t) return set_error(KITC_EINVAL, "kitc_modified_weights: NULL handle");
-    KITC_GUARD(return modified_weights(t, kernel, n, w, cb, ce, fhat, (cudaStream_t)s);)
+    KITC_GUARD(return modified_weights(t, kernel, n, w, cb, ce, &fhat, 1, (cudaStream_t)s);)
+}
+
+kitc_status kitc_modified_weights_peers(kitc_tree* t, int32_t kernel, int32_t n, const double* w, int64_t cb,
+                                        int64_t ce, double* const* fhat_peers, int32_t npeers, void* s) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_modified_weights_peers: NULL handle");
+    if (!fhat_peers) return set_error(KITC_EINVAL, "kitc_modified_weights_peers: NULL peer array");
+    KITC_GUARD(return modified_weights(t, kernel, n, w, cb, ce, fhat_peers, npeers, (cudaStream_t)s);)
 }
 
 kitc_status kitc_eval(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0, double eps,

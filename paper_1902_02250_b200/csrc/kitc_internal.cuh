@@ -12,6 +12,7 @@
 namespace kitc {
 
 constexpr int kMaxDegree = 16;        // n in [1, 16]
+constexpr int kMaxPeers = 8;          // fhat replicas written by one modified-weights call (GPUs per node)
 #ifndef KITC_GROUP
 #define KITC_GROUP 8
 #endif
@@ -108,7 +109,7 @@ namespace kitc {
 kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N, int32_t N0, cudaStream_t s);
 // weights.cu
 kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, int64_t cb,
-                             int64_t ce, double* fhat, cudaStream_t s);
+                             int64_t ce, double* const* fhat_peers, int npeers, cudaStream_t s);
 // eval.cu
 // A separate target set, Morton-sorted (targets.cu): coordinates SoA by sorted
 // position, the original row of each, count.  Batches are kBatch consecutive

@@ -37,6 +37,16 @@ struct Nodes {
     double t[kMaxDegree + 1];
 };
 
+// Destination replicas of fhat: the computed slice of every cluster is stored
+// into each of them (same layout and offsets).  n = 1: the caller's buffer; n > 1:
+// the fused modified-weights + all-gather of the multi-GPU path -- the other
+// entries are peer GPUs' buffers mapped into this process (symmetric memory over
+// NVLink), so the exchange is the kernel's own stores, with no separate collective.
+struct Peers {
+    double* p[kMaxPeers];
+    int n;
+};
+
 __global__ void k_gather_w(const double* __restrict__ w, const int* __restrict__ perm, int N, int m,
                            double* __restrict__ ws) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -91,7 +101,7 @@ template <int P, int M>
 __global__ void __launch_bounds__((P * P + 31) / 32 * 32) k_weights(
     const WItem* __restrict__ items, const double* __restrict__ x, const double* __restrict__ y,
     const double* __restrict__ z, const double* __restrict__ ws, int N, const double* __restrict__ grid,
-    double* __restrict__ fhat, double* __restrict__ part) {
+    const Peers fhat, double* __restrict__ part) {
     constexpr int P2 = P * P, NT = (P2 + 31) / 32 * 32, R = (P2 + kRows - 1) / kRows;
     constexpr int LEN = R * P * M * kRows;
     __shared__ double sg[3 * P];
@@ -131,20 +141,23 @@ __global__ void __launch_bounds__((P * P + 31) / 32 * 32) k_weights(
         }
         __syncthreads();
     }
-    double* dst = it.slot < 0 ? fhat + (size_t)it.c * LEN : part + (size_t)it.slot * LEN;
-    // zero padding rows P2 .. R kRows - 1
-    for (int q = tid; q < (R * kRows - P2) * P * M; q += NT) {
-        const int row = P2 + q / (P * M), km = q % (P * M);
-        dst[((row / kRows) * P * M + km) * kRows + row % kRows] = 0.0;
-    }
-    if (!owner) return;
-#pragma unroll
-    for (int m = 0; m < M; ++m)
-#pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) {
-            const int row = k1 * P + k2;
-            dst[(((row / kRows) * P + k3) * M + m) * kRows + row % kRows] = acc[m][k1];
+    const int nd = it.slot < 0 ? fhat.n : 1;
+    for (int r = 0; r < nd; ++r) {
+        double* dst = it.slot < 0 ? fhat.p[r] + (size_t)it.c * LEN : part + (size_t)it.slot * LEN;
+        // zero padding rows P2 .. R kRows - 1
+        for (int q = tid; q < (R * kRows - P2) * P * M; q += NT) {
+            const int row = P2 + q / (P * M), km = q % (P * M);
+            dst[((row / kRows) * P * M + km) * kRows + row % kRows] = 0.0;
         }
+        if (!owner) continue;
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+            for (int k1 = 0; k1 < P; ++k1) {
+                const int row = k1 * P + k2;
+                dst[(((row / kRows) * P + k3) * M + m) * kRows + row % kRows] = acc[m][k1];
+            }
+    }
 }
 
 struct RItem {
@@ -153,18 +166,18 @@ struct RItem {
 
 // fhat[c] = sum of its partial slots in chunk order (deterministic).
 __global__ void k_reduce(const RItem* __restrict__ r, int len, const double* __restrict__ part,
-                         double* __restrict__ fhat) {
+                         const Peers fhat) {
     const RItem it = r[blockIdx.x];
     for (int i = threadIdx.x; i < len; i += blockDim.x) {
         double s = part[(size_t)it.first_slot * len + i];
         for (int k = 1; k < it.nslots; ++k) s += part[(size_t)(it.first_slot + k) * len + i];
-        fhat[(size_t)it.c * len + i] = s;
+        for (int q = 0; q < fhat.n; ++q) fhat.p[q][(size_t)it.c * len + i] = s;
     }
 }
 
 template <int P, int M>
 static void launch_weights(int nitems, const WItem* items, const kitc_tree* t, const double* ws,
-                           const double* grid, double* fhat, double* part, cudaStream_t s) {
+                           const double* grid, const Peers& fhat, double* part, cudaStream_t s) {
     constexpr int NT = (P * P + 31) / 32 * 32;
     k_weights<P, M><<<nitems, NT, 0, s>>>(items, t->x.as<double>(), t->y.as<double>(), t->z.as<double>(), ws,
                                           (int)t->N, grid, fhat, part); note_launch();
@@ -172,7 +185,7 @@ static void launch_weights(int nitems, const WItem* items, const kitc_tree* t, c
 
 template <int M>
 static kitc_status dispatch(int n, int nitems, const WItem* items, const kitc_tree* t, const double* ws,
-                            const double* grid, double* fhat, double* part, cudaStream_t s) {
+                            const double* grid, const Peers& fhat, double* part, cudaStream_t s) {
     switch (n + 1) {
 #define KITC_W(P) \
     case P: launch_weights<P, M>(nitems, items, t, ws, grid, fhat, part, s); break;
@@ -187,13 +200,19 @@ static kitc_status dispatch(int n, int nitems, const WItem* items, const kitc_tr
 }  // namespace
 
 kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, int64_t cb, int64_t ce,
-                             double* fhat, cudaStream_t s) {
+                             double* const* fhat_peers, int npeers, cudaStream_t s) {
+    if (npeers < 1 || npeers > kMaxPeers) return set_error(KITC_EINVAL, "kitc_modified_weights: npeers out of range");
+    Peers fhat;
+    fhat.n = npeers;
+    for (int q = 0; q < kMaxPeers; ++q) fhat.p[q] = q < npeers ? fhat_peers[q] : nullptr;
+    for (int q = 0; q < npeers; ++q)
+        if (!fhat.p[q] && ce > cb) return set_error(KITC_EINVAL, "kitc_modified_weights: NULL buffer");
     int32_t m = 0, p = 0;
     KITC_TRY(kitc_kernel_dims(kernel, &m, &p));
     if (n < 1 || n > kMaxDegree) return set_error(KITC_EINVAL, "kitc_modified_weights: n must be in [1, 16]");
     if (!t->built) return set_error(KITC_ESTATE, "kitc_modified_weights: tree not built");
     if (cb < 0 || ce > t->nclusters || cb > ce) return set_error(KITC_EINVAL, "kitc_modified_weights: bad cluster range");
-    if (!w || (!fhat && ce > cb)) return set_error(KITC_EINVAL, "kitc_modified_weights: NULL buffer");
+    if (!w) return set_error(KITC_EINVAL, "kitc_modified_weights: NULL buffer");
     const int N = (int)t->N, C = (int)t->nclusters, P = n + 1;
     const long long LEN = fhat_cluster_len(P, m);
     // sorted weights (SoA, m planes)

@@ -4,10 +4,14 @@ Decomposition (DESIGN.md "Multi-GPU"):
   * every rank builds the same tree redundantly (deterministic, bit-exact);
   * modified weights are SHARDED: rank r computes clusters [cb_r, ce_r),
     contiguous ranges balanced by sum of N_C (Algorithm 1 costs O(n^3 N_C));
-  * ONE exchange step: an NCCL all-gather replicates fhat over NVLink (shards
-    padded to equal size, gathered in place, then placed at their cluster
-    offsets with device-to-device copies);
-  * targets are partitioned by 32-target batches, contiguous ranges balanced
+  * ONE exchange step, fused into the modified-weights kernel: fhat lives in
+    symmetric memory (one buffer per GPU, every peer's buffer mapped into every
+    process over NVLink 5 / NVSwitch) and each rank's kernel stores its
+    clusters' slices into ALL replicas (kitc_modified_weights_peers), bracketed
+    by two device-side barriers (PeerFhat).  The baseline exchange -- an NCCL
+    all-gather of padded shards placed at their cluster offsets
+    (all_gather_fhat) -- stays available and is the bench's cross-check;
+  * targets are partitioned by warp batches (<= 4 targets of one leaf), contiguous ranges balanced
     by target count; outputs stay sharded (each rank writes its targets).
 Per-target traversal and summation orders do not depend on the partition, so
 outputs are bitwise identical for any number of ranks.
@@ -61,3 +65,32 @@ def all_gather_fhat(fhat_full, gathered, shard, shards, rank, group=None):
         if e > b:
             fhat_full[b:e].copy_(gathered[r, : e - b])
     return fhat_full
+
+
+class PeerFhat:
+    """Fused modified weights + all-gather over peer memory.
+
+    fhat [C, L] is allocated in torch symmetric memory; rendezvous maps every
+    rank's buffer into every process.  modified_weights() runs, on the caller's
+    stream: barrier (every rank has finished reading the previous fhat) ->
+    kitc_modified_weights_peers(this rank's clusters -> all replicas) ->
+    barrier (every replica complete).  No separate collective; the exchange is
+    the kernel's own NVLink stores, overlapped with its compute."""
+
+    def __init__(self, C, L, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.fhat = symm.empty((C, L), dtype=torch.float64, device=device)
+        self.hdl = symm.rendezvous(self.fhat, group if group is not None else dist.group.WORLD)
+        off = int(getattr(self.hdl, "offset", 0) or 0)
+        self.ptrs = [int(p) + off for p in self.hdl.buffer_ptrs]
+        assert self.ptrs[self.hdl.rank] == self.fhat.data_ptr(), "symmetric memory: unexpected local mapping"
+
+    def modified_weights(self, T, kernel, n, W, cluster_range, stream=None):
+        from . import kitc
+        cb, ce = cluster_range
+        self.hdl.barrier(channel=0)
+        kitc.kitc_modified_weights_peers(T.handle, kernel, n, kitc._ptr(W), cb, ce, self.ptrs, kitc._stream(stream))
+        self.hdl.barrier(channel=0)
+        return self.fhat

@@ -29,7 +29,7 @@ KERNELS = {"stokeslet": STOKESLET, "rotlet": ROTLET, "stokeslet_rotlet": STOKESL
 
 # every symbol include/kitc.h declares
 EXPORTS = ("kitc_kernel_dims", "kitc_fhat_cluster_len", "kitc_tree_create", "kitc_build_tree", "kitc_tree_info",
-           "kitc_tree_export", "kitc_modified_weights", "kitc_eval", "kitc_eval_ex", "kitc_eval_targets", "kitc_eval_targets_ex", "kitc_batch_targets",
+           "kitc_tree_export", "kitc_modified_weights", "kitc_modified_weights_peers", "kitc_eval", "kitc_eval_ex", "kitc_eval_targets", "kitc_eval_targets_ex", "kitc_batch_targets",
            "kitc_direct", "kitc_direct_sample", "kitc_rel_error", "kitc_tree_free", "kitc_last_error",
            "kitc_launch_count")
 
@@ -53,6 +53,7 @@ def _load():
         "kitc_tree_info": [vp, P(i64), P(i32), P(i64), P(i32)],
         "kitc_tree_export": [vp] + [vp] * 9,
         "kitc_modified_weights": [vp, i32, i32, vp, i64, i64, vp, vp],
+        "kitc_modified_weights_peers": [vp, i32, i32, vp, i64, i64, vp, i32, vp],
         "kitc_fhat_cluster_len": [i32, i32, P(i64)],
         "kitc_eval": [vp, i32, i32, d, i32, d, i32, vp, i64, i64, vp, vp, vp],
         "kitc_eval_ex": [vp, i32, i32, d, i32, d, i32, C.c_uint32, vp, i64, i64, vp, vp, vp],
@@ -149,6 +150,13 @@ def kitc_eval(t, kernel, n, theta, N0, eps, self_mode, fhat_ptr, batch_begin, ba
     return _call("kitc_eval", t, int(kernel), int(n), float(theta), int(N0), float(eps),
                  int(self_mode), fhat_ptr, int(batch_begin), int(batch_end), out_ptr, stats_ptr,
                  stream_ptr)
+
+
+def kitc_modified_weights_peers(t, kernel, n, w_ptr, cluster_begin, cluster_end, peer_ptrs, stream_ptr):
+    """peer_ptrs: sequence of device addresses (int) of the fhat replicas to write."""
+    arr = (C.c_void_p * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
+    return _call("kitc_modified_weights_peers", t, int(kernel), int(n), w_ptr, int(cluster_begin),
+                 int(cluster_end), C.cast(arr, C.c_void_p), len(peer_ptrs), stream_ptr)
 
 
 def kitc_eval_ex(t, kernel, n, theta, N0, eps, self_mode, flags, fhat_ptr, batch_begin, batch_end, out_ptr,

@@ -121,3 +121,49 @@ def test_size_check_parity(K, N, N0, n, kern):
     got_t, gst_t = G.eval_targets(kern, n, 0.7, 0.01, fh, dev(Xt), stats=True, size_check=True)
     assert O.rel_error(ref_t, host(got_t)) <= TREE_GATE
     assert np.array_equal(rst_t.astype(np.int64), host(gst_t))
+
+
+def test_modified_weights_peers_replicas(K):
+    # the fused weights + exchange kernel writes every cluster slice into each replica
+    # (here: three local buffers standing in for peer GPUs' mapped buffers)
+    X, W = KI.particles(30000, seed=5)
+    G = K.Tree(dev(X), 400)
+    ref = G.modified_weights(0, 6, dev(W))
+    reps = [torch.full_like(ref, float("nan")) for _ in range(3)]
+    C = G.nclusters
+    for cb, ce in [(0, C // 3), (C // 3, C)]:           # two "ranks"' cluster ranges
+        K.kitc_modified_weights_peers(G.handle, 0, 6, K._ptr(dev(W)), cb, ce, [r.data_ptr() for r in reps],
+                                      K._stream())
+    for r in reps:
+        assert torch.equal(r, ref)
+    with pytest.raises(K.KitcError):
+        K.kitc_modified_weights_peers(G.handle, 0, 6, K._ptr(dev(W)), 0, C, [reps[0].data_ptr()] * 9, K._stream())
+
+
+def test_peer_fhat_world1(K):
+    # dist.PeerFhat (symmetric memory + device barriers) on a one-rank NCCL group
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1902_02250_b200 import dist as D
+    own = not dist.is_initialized()
+    if own:
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        X, W = KI.particles(20000, seed=6)
+        G = K.Tree(dev(X), 300)
+        ref = G.modified_weights(0, 5, dev(W))
+        pf = D.PeerFhat(G.nclusters, ref.shape[1], torch.device("cuda", 0))
+        for _ in range(2):                               # the barriers are reusable across steps
+            got = pf.modified_weights(G, 0, 5, dev(W), (0, G.nclusters))
+        torch.cuda.synchronize()
+        assert torch.equal(got, ref)
+        assert torch.equal(G.eval(0, 5, 0.7, 0.01, got), G.eval(0, 5, 0.7, 0.01, ref))
+    finally:
+        if own:
+            dist.destroy_process_group()
