@@ -206,11 +206,17 @@ def run_kitc(args, cfg, rank, world, local_rank):
                                    kitc._stream())
         D.all_gather_fhat(fhat, gathered, gathered[rank], cshards, rank)
 
-    exchange = "none (1 GPU)"
-    if world > 1 and args.exchange == "p2p":
+    exchange = "none (1 GPU)" if world == 1 else "NCCL all_gather_into_tensor of padded fhat shards"
+    use_p2p = world > 1 and args.exchange == "p2p"
+    if use_p2p:
         # fused weights + exchange over peer memory; cross-checked bitwise against the NCCL path
-        pf = D.PeerFhat(C, L, dev)
-        fhat_p2p = pf.modified_weights(T, kern, n, Wd, (cb, ce))
+        try:
+            pf = D.PeerFhat(C, L, dev)
+            fhat_p2p = pf.modified_weights(T, kern, n, Wd, (cb, ce))
+        except Exception as ex:  # symmetric memory unavailable on this node: say so, use NCCL
+            use_p2p = False
+            exchange = f"NCCL all_gather_into_tensor (peer-memory path unavailable: {type(ex).__name__}: {ex})"[:300]
+    if use_p2p:
         weights_nccl()
         torch.cuda.synchronize()
         ok = torch.tensor([int(torch.equal(fhat_p2p[1:], fhat[1:]))], device=dev)
@@ -219,13 +225,11 @@ def run_kitc(args, cfg, rank, world, local_rank):
             raise RuntimeError("fused peer-memory fhat differs from the NCCL all-gather")
         fhat = fhat_p2p
         exchange = f"fused modified weights -> {world} peer replicas (symmetric memory, device barriers)"
-    elif world > 1:
-        exchange = "NCCL all_gather_into_tensor of padded fhat shards"
 
     def weights():
         if world == 1:
             T.modified_weights(kern, n, Wd, cluster_range=(cb, ce), fhat=fhat)
-        elif args.exchange == "p2p":
+        elif use_p2p:
             pf.modified_weights(T, kern, n, Wd, (cb, ce))
         else:
             weights_nccl()
