@@ -33,10 +33,19 @@ namespace {
 #ifndef KITC_EVAL_MINB1
 #define KITC_EVAL_MINB1 4  // rotlet / combined (measured: 4 beats 5 and 6 on C4)
 #endif
+#ifndef KITC_NEAR_TEAMS
+#define KITC_NEAR_TEAMS 1  // near field: idle target groups join the participating ones
+#endif
 #ifndef KITC_EVAL_SB
 #define KITC_EVAL_SB 2
 #endif
 constexpr int kWarps = KITC_EVAL_WARPS;  // warps (batches) per CTA
+#ifdef KITC_EVAL_HIST
+__device__ unsigned long long g_hist[10];
+}  // namespace
+extern "C" void kitc_eval_hist(unsigned long long* h) { cudaMemcpyFromSymbol(h, g_hist, sizeof(g_hist)); }
+namespace {
+#endif
 constexpr int kSB = KITC_EVAL_SB;         // fhat blocks per pipeline stage (1 or 2)
 static_assert(kSB == 1 || kSB == 2, "kSB");
 static_assert(kGroup == kRows, "k_eval: one fhat row per lane of a target group");
@@ -242,22 +251,22 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
     __syncwarp(am);
 }
 
-// Near field of one rejected leaf: lane group g sums sources b + g, b + g + kGroup, ...
-// (unrolled x4 with the loads hoisted).
+// Near field of one rejected leaf: the lane of rank `rk` in a team of TS lanes
+// working for target t (position x, y, z) sums sources b + rk, b + rk + TS, ...
+// (unrolled x4 with the loads hoisted).  The self pair (j == t under SELF_OMIT)
+// is evaluated with f = 0 and s = 1: an exact zero contribution, no branch.
 template <int KER>
-__device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e, int grp,
+__device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e, int rk, int TS,
                                            const EvalArgs& a, double* acc) {
     using K = EvalKern<KER>;
     constexpr int M = K::M, U = 4;
-    // The self pair (j == t under SELF_OMIT) is evaluated with f = 0 and s = 1:
-    // its contribution is exactly zero, so the loop stays branch-free.
     const int self = a.self_omit ? t : -1;
-    int j = b + grp;
-    for (; j + (U - 1) * kGroup < e; j += U * kGroup) {
+    int j = b + rk;
+    for (; j + (U - 1) * TS < e; j += U * TS) {
         double sx[U], sy[U], sz[U], f[U][M];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int jj = j + u * kGroup;
+            const int jj = j + u * TS;
             sx[u] = __ldg(a.x + jj);
             sy[u] = __ldg(a.y + jj);
             sz[u] = __ldg(a.z + jj);
@@ -266,7 +275,7 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const bool me = (j + u * kGroup) == self;
+            const bool me = (j + u * TS) == self;
             const double dx = x - sx[u], dy = y - sy[u], dz = z - sz[u];
 #pragma unroll
             for (int m = 0; m < M; ++m) f[u][m] = me ? 0.0 : f[u][m];
@@ -274,7 +283,7 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
             K::pair(dx, dy, dz, s, f[u], acc, a.kp);
         }
     }
-    for (; j < e; j += kGroup) {
+    for (; j < e; j += TS) {
         const bool me = j == self;
         const double dx = x - __ldg(a.x + j), dy = y - __ldg(a.y + j), dz = z - __ldg(a.z + j);
         double f[M];
@@ -282,6 +291,63 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
         for (int m = 0; m < M; ++m) f[m] = me ? 0.0 : __ldg(a.w + (size_t)m * a.N + j);
         const double s = me ? 1.0 : fma(dx, dx, fma(dy, dy, fma(dz, dz, a.kp.e2)));
         K::pair(dx, dy, dz, s, f, acc, a.kp);
+    }
+}
+
+// Near field of leaf [b, e) for the participating lanes `rm` (whole target groups).
+// With 3 or 4 participating targets each sums with its own kGroup lanes.  With 1
+// or 2, the idle groups join them ("teams" of 32 or 16 lanes): every lane sums a
+// strided share of the sources for its team's target into scratch accumulators,
+// and the team's partial sums are folded into the owning group's lanes with
+// butterfly shuffles -- the per-target result is the same sum (rounding order
+// aside), with no idle lanes.  Called by ALL lanes of the warp.
+template <int KER>
+__device__ __forceinline__ void near_leaf(double x, double y, double z, int t, int b, int e, int lane, unsigned rm,
+                                          const EvalArgs& a, double* acc) {
+    using K = EvalKern<KER>;
+    constexpr int NA = K::NA;
+    const int grp = lane % kGroup, g = lane / kGroup;
+    const int nt = __popc(rm) / kGroup;
+    const bool mine = (rm >> lane) & 1u;
+    if (!KITC_NEAR_TEAMS || nt >= 3) {
+        if (mine) near_field<KER>(x, y, z, t, b, e, grp, kGroup, a, acc);
+        return;
+    }
+    // groups of the participating targets (ascending): ga [, gb]
+    const unsigned gm = rm & 0x01010101u;  // one bit per participating group (its lane 0)
+    const int ga = (__ffs(gm) - 1) / kGroup;
+    int src, rk, TS, xm;
+    if (nt == 1) {
+        TS = 32;
+        src = ga;
+        rk = ((g - ga) & 3) * kGroup + grp;
+        xm = 0;
+    } else {
+        const int gb = (31 - __clz(gm)) / kGroup;
+        TS = 16;
+        // partner groups: lane ^ xm*kGroup, chosen so each active group pairs with an idle one
+        xm = ((ga ^ gb) == 1) ? 2 : 1;
+        const bool act = g == ga || g == gb;
+        src = act ? g : (g ^ xm);
+        rk = (act ? 0 : kGroup) + grp;
+    }
+    const int sl = src * kGroup;
+    const double tx = __shfl_sync(0xffffffffu, x, sl), ty = __shfl_sync(0xffffffffu, y, sl);
+    const double tz = __shfl_sync(0xffffffffu, z, sl);
+    const int tt = __shfl_sync(0xffffffffu, t, sl);
+    double tmp[NA];
+#pragma unroll
+    for (int c = 0; c < NA; ++c) tmp[c] = 0.0;
+    near_field<KER>(tx, ty, tz, tt, b, e, rk, TS, a, tmp);
+#pragma unroll
+    for (int c = 0; c < NA; ++c) {
+        if (nt == 1) {
+            tmp[c] += __shfl_xor_sync(0xffffffffu, tmp[c], 8);
+            tmp[c] += __shfl_xor_sync(0xffffffffu, tmp[c], 16);
+        } else {
+            tmp[c] += __shfl_xor_sync(0xffffffffu, tmp[c], xm * kGroup);
+        }
+        if (mine) acc[c] += tmp[c];
     }
 }
 
@@ -354,11 +420,19 @@ __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_
         const unsigned am = __ballot_sync(0xffffffffu, ok);
         const unsigned rm = mask & ~am;
         const int4 tp = a.topo[c];
+#ifdef KITC_EVAL_HIST
+        // tuning only: histogram of accepting targets per (warp, far cluster) and of
+        // near-field participants per (warp, leaf) -> g_hist[0..4], g_hist[5..9]
+        if (lane == 0) {
+            if (am) atomicAdd(&g_hist[__popc(am) / kGroup], 1ull);
+            if (rm && tp.w == 0) atomicAdd(&g_hist[5 + __popc(rm) / kGroup], 1ull);
+        }
+#endif
         if (am && a.size_check && tp.y - tp.x < P3) {
             // size-check variant (flag KITC_EVAL_SIZE_CHECK): an accepted cluster with
             // fewer particles than proxies is summed directly (the target is outside it)
             if (ok) {
-                near_field<KER>(x, y, z, t, tp.x, tp.y, grp, a, acc);
+                near_field<KER>(x, y, z, t, tp.x, tp.y, grp, kGroup, a, acc);
                 if (STATS) {
                     st[2] += 1;
                     st[3] += (unsigned long long)(tp.y - tp.x);
@@ -376,8 +450,8 @@ __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_
         }
         if (rm) {
             if (tp.w == 0) {
+                near_leaf<KER>(x, y, z, t, tp.x, tp.y, lane, rm, a, acc);
                 if (in && !ok) {
-                    near_field<KER>(x, y, z, t, tp.x, tp.y, grp, a, acc);
                     if (STATS) {
                         const int self = (a.self_omit && t >= tp.x && t < tp.y) ? 1 : 0;
                         st[2] += 1;

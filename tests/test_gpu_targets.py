@@ -59,13 +59,15 @@ def test_eval_targets_parity(K, N, N0, n, theta, kern, eps, geom, nt, spread):
 
 
 def test_eval_targets_equals_self_include_on_sources(K):
-    # targets = sources: per-target results do not depend on the batching -> bitwise equal
+    # targets = sources: same interaction lists (integers equal); the sums differ only in
+    # rounding order (near-field lane teams depend on the batch-mates)
     X, W = KI.particles(20000, seed=3)
     G = K.Tree(dev(X), 300)
     fh = G.modified_weights(0, 7, dev(W))
-    a = G.eval(0, 7, 0.7, 0.01, fh, self_omit=False)
-    b = G.eval_targets(0, 7, 0.7, 0.01, fh, dev(X))
-    assert torch.equal(a, b)
+    a, sa = G.eval(0, 7, 0.7, 0.01, fh, self_omit=False, stats=True)
+    b, sb = G.eval_targets(0, 7, 0.7, 0.01, fh, dev(X), stats=True)
+    assert torch.equal(sa, sb)
+    assert float((a - b).norm() / a.norm()) < 1e-13
 
 
 def test_eval_targets_empty_and_errors(K):
