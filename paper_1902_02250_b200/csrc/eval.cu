@@ -36,6 +36,9 @@ namespace {
 #ifndef KITC_NEAR_TEAMS
 #define KITC_NEAR_TEAMS 1  // near field: idle target groups join the participating ones
 #endif
+#ifndef KITC_FAR_TEAMS
+#define KITC_FAR_TEAMS 1  // far field: idle target groups join 1 or 2 accepting targets
+#endif
 #ifndef KITC_EVAL_SB
 #define KITC_EVAL_SB 2
 #endif
@@ -251,6 +254,147 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
     __syncwarp(am);
 }
 
+// Far field of one cluster accepted by only 1 or 2 of the batch's targets, by the
+// WHOLE warp ("teams", as near_leaf): the idle target groups join the accepting
+// ones.  Two targets: teams of 16 lanes, one row of the 16-row stage per lane.
+// One target: 32 lanes, each row split between two lanes by k3 halves (the row
+// sums of EvalKern::pair_row are linear, so partial rows fold like full ones).
+// Same TMA-staged double buffer and round counter as far_field; partial sums are
+// folded into the accepting groups' lanes with butterfly shuffles.
+template <int PT, int KER>
+__device__ __forceinline__ void far_field_team(double x, double y, double z, const double* __restrict__ g,
+                                               const double* __restrict__ F, double* acc, const KParams& kp,
+                                               int Prt, int lane, unsigned am, const WarpSmem& ws) {
+    using K = EvalKern<KER>;
+    constexpr int M = K::M, NA = K::NA;
+    const int P = PT > 0 ? PT : Prt, P2 = P * P;
+    const int R = (P2 + kRows - 1) / kRows, RF = P2 / kRows;
+    const int blk = P * M * kRows;
+    const int NS = (R + kSB - 1) / kSB;
+    const int grp = lane % kGroup, gl = lane / kGroup;
+    const bool mine = (am >> lane) & 1u;
+    const unsigned gm = am & 0x01010101u;
+    const int nt = __popc(gm);
+    const int ga = (__ffs(gm) - 1) / kGroup;
+    int src, rk, TS, xm;
+    if (nt == 1) {
+        TS = 32;
+        src = ga;
+        rk = ((gl - ga) & 3) * kGroup + grp;
+        xm = 0;
+    } else {
+        const int gb = (31 - __clz(gm)) / kGroup;
+        TS = 16;
+        xm = ((ga ^ gb) == 1) ? 2 : 1;
+        const bool act = gl == ga || gl == gb;
+        src = act ? gl : (gl ^ xm);
+        rk = (act ? 0 : kGroup) + grp;
+    }
+    const int sl = src * kGroup;
+    const double tx = __shfl_sync(0xffffffffu, x, sl), ty = __shfl_sync(0xffffffffu, y, sl);
+    const double tz = __shfl_sync(0xffffffffu, z, sl);
+    const int base = *ws.nround;
+    auto issue = [&](int st, int k) {
+        const int nb = min(kSB, R - st * kSB);
+        tma_round(ws.buf + (k & 1) * kSB * blk, F + (size_t)st * kSB * blk, (unsigned)(nb * blk * 8),
+                  ws.bar + (k & 1));
+    };
+    if (lane == 0) {
+        issue(0, base);
+        if (NS > 1) issue(1, base + 1);
+    }
+    // this lane's rows: row j of block h of every stage; one target: k3 in [klo, klo + KH)
+    const int r16 = rk & 15, h = r16 >> 3, j = r16 & 7;
+    constexpr int KH = PT > 0 ? (PT + 1) / 2 : 1;
+    const int khalf = (P + 1) / 2;
+    const int klo = (TS == 32 && rk >= 16) ? khalf : 0;
+    const int kn = TS == 32 ? (rk >= 16 ? P - khalf : khalf) : P;  // k3 count of this lane's rows
+    double tmp[NA];
+#pragma unroll
+    for (int c = 0; c < NA; ++c) tmp[c] = 0.0;
+    double dzh[PT > 0 ? PT : 1];
+    if constexpr (PT > 0) {
+#pragma unroll
+        for (int i = 0; i < PT; ++i) dzh[i] = tz - __ldg(g + 2 * PT + min(klo + i, PT - 1));
+    }
+    for (int st = 0; st < NS; ++st) {
+        const int k = base + st;
+        const double* B = ws.buf + (k & 1) * kSB * blk;
+        mbar_wait(ws.bar + (k & 1), (unsigned)(k >> 1) & 1u);
+        const int b0 = st * kSB, bb = b0 + h;
+        if (bb < RF) {
+            const int row = bb * kRows + j;
+            const int k1 = row / P, k2 = row - k1 * P;
+            const double dx = tx - __ldg(g + k1), dy = ty - __ldg(g + P + k2);
+            const double pxye = fma(dy, dy, dx * dx) + kp.e2;
+            const double* Bj = B + h * blk + j;
+            typename K::Row r;
+            if constexpr (PT > 0) {
+                if (TS == 16) {
+#pragma unroll
+                    for (int k3 = 0; k3 < PT; ++k3) {
+                        double f[M];
+#pragma unroll
+                        for (int m = 0; m < M; ++m) f[m] = Bj[(k3 * M + m) * kRows];
+                        K::pair_row(dx, dy, dzh[k3], fma(dzh[k3], dzh[k3], pxye), f, tmp,
+                                    r, kp);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < KH; ++i) {
+                        if (i < kn) {
+                            double f[M];
+#pragma unroll
+                            for (int m = 0; m < M; ++m) f[m] = Bj[((klo + i) * M + m) * kRows];
+                            K::pair_row(dx, dy, dzh[i], fma(dzh[i], dzh[i], pxye), f, tmp, r, kp);
+                        }
+                    }
+                }
+            } else {
+                for (int i = 0; i < kn; ++i) {
+                    const int k3 = klo + i;
+                    const double dzk = tz - __ldg(g + 2 * P + k3);
+                    double f[M];
+#pragma unroll
+                    for (int m = 0; m < M; ++m) f[m] = Bj[(k3 * M + m) * kRows];
+                    K::pair_row(dx, dy, dzk, fma(dzk, dzk, pxye), f, tmp, r, kp);
+                }
+            }
+            K::row_end(dx, dy, r, tmp);
+        }
+        if (RF < R && RF >= b0 && RF < b0 + kSB) {  // the partial last block, pair by pair
+            const double* Bb = B + (RF - b0) * blk;
+            const int pairs = (P2 - RF * kRows) * P;
+            for (int q = rk; q < pairs; q += TS) {
+                const int jj = q / P, k3 = q - jj * P, row = RF * kRows + jj;
+                const int k1 = row / P, k2 = row - k1 * P;
+                const double dx = tx - __ldg(g + k1), dy = ty - __ldg(g + P + k2), dzk = tz - __ldg(g + 2 * P + k3);
+                double f[M];
+#pragma unroll
+                for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + jj];
+                K::pair(dx, dy, dzk, fma(dy, dy, dx * dx) + fma(dzk, dzk, kp.e2), f, tmp, kp);
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && st + 2 < NS) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(st + 2, k);
+        }
+    }
+    if (lane == 0) *ws.nround = base + NS;
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < NA; ++c) {
+        if (nt == 1) {
+            tmp[c] += __shfl_xor_sync(0xffffffffu, tmp[c], 8);
+            tmp[c] += __shfl_xor_sync(0xffffffffu, tmp[c], 16);
+        } else {
+            tmp[c] += __shfl_xor_sync(0xffffffffu, tmp[c], xm * kGroup);
+        }
+        if (mine) acc[c] += tmp[c];
+    }
+}
+
 // Near field of one rejected leaf: the lane of rank `rk` in a team of TS lanes
 // working for target t (position x, y, z) sums sources b + rk, b + rk + TS, ...
 // (unrolled x4 with the loads hoisted).  The self pair (j == t under SELF_OMIT)
@@ -438,6 +582,14 @@ __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_
                     st[3] += (unsigned long long)(tp.y - tp.x);
                     st[4] += (unsigned long long)(tp.y - tp.x);
                 }
+            }
+        } else if (am && KITC_FAR_TEAMS && kSB == 2 && __popc(am) <= 2 * kGroup) {
+            far_field_team<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * LEN, acc, a.kp, P,
+                                    lane, am, ws);
+            if (STATS && ok) {
+                st[0] += 1;
+                st[1] += (unsigned long long)P3;
+                st[4] += (unsigned long long)(tp.y - tp.x);
             }
         } else if (am && ok) {
             far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * LEN, acc, a.kp, P, grp,
