@@ -194,6 +194,17 @@ kitc_status kitc_eval_targets_ex(const kitc_tree* t, int32_t kernel, int32_t n, 
                                  double eps, uint32_t flags, const double* fhat_dev, const double* xt_dev,
                                  int64_t Nt, double* out_dev, uint64_t* stats_dev, void* s);
 
+/* kitc_eval_ex for part `part` of an interleaved split of ALL batches into
+ * nparts parts (multi-GPU: part = rank, nparts = world size): the batches come
+ * in chunks of 64 dealt round-robin, so every part samples the whole domain and
+ * the parts' work is balanced (contiguous ranges balanced by target count leave
+ * up to 7% imbalance, tools/balance_check.py).  The batches themselves do not
+ * change, so every target's result is bitwise that of the single-GPU run.
+ *  0 <= part < nparts.  Other arguments as kitc_eval_ex. */
+kitc_status kitc_eval_part(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0, double eps,
+                           int32_t self, uint32_t flags, const double* fhat_dev, int32_t part, int32_t nparts,
+                           double* out_dev, uint64_t* stats_dev, void* s);
+
 /* Number of targets in batches [0, batch_end) -- for splitting work. */
 kitc_status kitc_batch_targets(const kitc_tree* t, int64_t batch_end, int64_t* n_targets);
 

@@ -117,6 +117,15 @@ kitc_status kitc_eval(const kitc_tree* t, int32_t kernel, int32_t n, double thet
     KITC_GUARD(return eval(t, kernel, n, theta, eps, self, fhat, bb, be, out, stats, (cudaStream_t)s);)
 }
 
+kitc_status kitc_eval_part(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0, double eps,
+                           int32_t self, uint32_t flags, const double* fhat, int32_t part, int32_t nparts,
+                           double* out, uint64_t* stats, void* s) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_eval_part: NULL handle");
+    if (t->built && N0 != t->N0) return set_error(KITC_EINVAL, "kitc_eval_part: N0 differs from the tree's N0");
+    KITC_GUARD(return eval(t, kernel, n, theta, eps, self, fhat, 0, t->nbatches, out, stats, (cudaStream_t)s,
+                           nullptr, flags, part, nparts);)
+}
+
 kitc_status kitc_eval_ex(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0, double eps,
                          int32_t self, uint32_t flags, const double* fhat, int64_t bb, int64_t be, double* out,
                          uint64_t* stats, void* s) {

@@ -43,6 +43,7 @@ namespace {
 #define KITC_EVAL_SB 2
 #endif
 constexpr int kWarps = KITC_EVAL_WARPS;  // warps (batches) per CTA
+constexpr int kPartChunk = 64;          // batches per chunk of the interleaved multi-GPU split
 #ifdef KITC_EVAL_HIST
 __device__ unsigned long long g_hist[10];
 }  // namespace
@@ -73,6 +74,7 @@ struct EvalArgs {
     double* out;
     unsigned long long* stats;
     long long bb, be;
+    int part, nparts;  // interleaved multi-GPU split (nparts > 1): chunks of kPartChunk batches
     int N;
     int P;  // n + 1 (runtime copy)
     int stack_cap;
@@ -523,7 +525,11 @@ __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_
         __syncwarp();
     }
     int2* stk = ws.stk;
-    const long long b = a.bb + (long long)blockIdx.x * kWarps + wl;
+    long long b = a.bb + (long long)blockIdx.x * kWarps + wl;
+    if (a.nparts > 1) {  // part-local index -> global batch of the interleaved chunks
+        const long long i = b;
+        b = ((i / kPartChunk) * a.nparts + a.part) * kPartChunk + i % kPartChunk;
+    }
     if (b >= a.be) return;  // whole warp
     int p0, tc;
     if (a.bstart) {
@@ -668,7 +674,8 @@ static void dispatch(int P, const EvalArgs& a, int grid, size_t smem, cudaStream
 
 kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps, int self, const double* fhat,
                  int64_t bb, int64_t be, double* out, uint64_t* stats, cudaStream_t s, const TargetSet* ts,
-                 unsigned flags) {
+                 unsigned flags, int part, int nparts) {
+    if (nparts < 1 || part < 0 || part >= nparts) return set_error(KITC_EINVAL, "kitc_eval: bad part / nparts");
     if (flags & ~(unsigned)KITC_EVAL_SIZE_CHECK) return set_error(KITC_EINVAL, "kitc_eval: unknown flags");
     if (!t->built) return set_error(KITC_ESTATE, "kitc_eval: tree not built");
     if (!t->weights_ready || t->grid_n != n || t->weights_kernel != kernel)
@@ -713,6 +720,8 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     a.stats = reinterpret_cast<unsigned long long*>(stats);
     a.bb = bb;
     a.be = be;
+    a.part = part;
+    a.nparts = nparts;
     a.N = (int)t->N;
     a.P = n + 1;
     a.stack_cap = 8 * (t->depth + 1);
@@ -728,7 +737,15 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
                          127) / 128 * 128);
     const size_t smem = (size_t)kWarps * a.warp_smem;
     if (smem > 200 * 1024) return set_error(KITC_EINVAL, "kitc_eval: tree too deep for the traversal stack");
-    const long long nb = be - bb;
+    long long nb = be - bb;
+    if (nparts > 1) {  // batches [0, be) split into chunks dealt round-robin; this part's count
+        if (bb != 0) return set_error(KITC_EINVAL, "kitc_eval: an interleaved split covers batches [0, end)");
+        const long long nch = (be + kPartChunk - 1) / kPartChunk;
+        nb = 0;
+        for (long long c = part; c < nch; c += nparts) nb += std::min<long long>(kPartChunk, be - c * kPartChunk);
+        if (nb == 0) return KITC_OK;
+        nb = ((nch - 1 - part) / nparts) * kPartChunk + kPartChunk;  // part-local index range (last chunk may be short)
+    }
     const int grid = (int)((nb + kWarps - 1) / kWarps);
     switch (kernel) {
         case KITC_STOKESLET: dispatch<0>(n + 1, a, grid, smem, s); break;

@@ -121,7 +121,8 @@ struct TargetSet {
 };
 kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps, int self,
                  const double* fhat, int64_t bb, int64_t be, double* out, uint64_t* stats,
-                 cudaStream_t s, const TargetSet* ts = nullptr, unsigned flags = 0);
+                 cudaStream_t s, const TargetSet* ts = nullptr, unsigned flags = 0, int part = 0,
+                 int nparts = 1);
 // targets.cu
 kitc_status eval_targets(const kitc_tree* t, int kernel, int n, double theta, double eps,
                          const double* fhat, const double* xt, int64_t Nt, double* out,

@@ -29,7 +29,7 @@ KERNELS = {"stokeslet": STOKESLET, "rotlet": ROTLET, "stokeslet_rotlet": STOKESL
 
 # every symbol include/kitc.h declares
 EXPORTS = ("kitc_kernel_dims", "kitc_fhat_cluster_len", "kitc_tree_create", "kitc_build_tree", "kitc_tree_info",
-           "kitc_tree_export", "kitc_modified_weights", "kitc_modified_weights_peers", "kitc_eval", "kitc_eval_ex", "kitc_eval_targets", "kitc_eval_targets_ex", "kitc_batch_targets",
+           "kitc_tree_export", "kitc_modified_weights", "kitc_modified_weights_peers", "kitc_eval", "kitc_eval_ex", "kitc_eval_part", "kitc_eval_targets", "kitc_eval_targets_ex", "kitc_batch_targets",
            "kitc_direct", "kitc_direct_sample", "kitc_rel_error", "kitc_tree_free", "kitc_last_error",
            "kitc_launch_count")
 
@@ -57,6 +57,7 @@ def _load():
         "kitc_fhat_cluster_len": [i32, i32, P(i64)],
         "kitc_eval": [vp, i32, i32, d, i32, d, i32, vp, i64, i64, vp, vp, vp],
         "kitc_eval_ex": [vp, i32, i32, d, i32, d, i32, C.c_uint32, vp, i64, i64, vp, vp, vp],
+        "kitc_eval_part": [vp, i32, i32, d, i32, d, i32, C.c_uint32, vp, i32, i32, vp, vp, vp],
         "kitc_eval_targets": [vp, i32, i32, d, i32, d, vp, vp, i64, vp, vp, vp],
         "kitc_eval_targets_ex": [vp, i32, i32, d, i32, d, C.c_uint32, vp, vp, i64, vp, vp, vp],
         "kitc_batch_targets": [vp, i64, P(i64)],
@@ -235,12 +236,18 @@ class Tree:
         return fhat
 
     def eval(self, kernel, n, theta, eps, fhat, out=None, batch_range=None, self_omit=True,
-             stats=False, stream=None, size_check=False):
+             stats=False, stream=None, size_check=False, part=None):
+        """part=(p, k): interleaved part p of k (kitc_eval_part) instead of a batch range."""
         _, p = kitc_kernel_dims(kernel)
         dev = fhat.device
         if out is None:
             out = torch.zeros((self.N, p), dtype=torch.float64, device=dev)
         st = torch.zeros((self.N, 5), dtype=torch.int64, device=dev) if stats else None
+        if part is not None:
+            _call("kitc_eval_part", self._h, int(kernel), int(n), float(theta), self.N0, float(eps),
+                  SELF_OMIT if self_omit else SELF_INCLUDE, C.c_uint32(EVAL_SIZE_CHECK if size_check else 0),
+                  _ptr(fhat), int(part[0]), int(part[1]), _ptr(out), _ptr(st), _stream(stream))
+            return (out, st) if stats else out
         bb, be = batch_range if batch_range is not None else (0, self.nbatches)
         kitc_eval_ex(self._h, kernel, n, theta, self.N0, eps, SELF_OMIT if self_omit else SELF_INCLUDE,
                      EVAL_SIZE_CHECK if size_check else 0, _ptr(fhat), bb, be, _ptr(out), _ptr(st), _stream(stream))

@@ -182,6 +182,12 @@ def test_split_ranges_bitwise_identical(K):
     for bb, be in [(0, 17), (17, nb // 2), (nb // 2, nb)]:
         G.eval(0, 6, 0.7, 0.01, parts, out=out, batch_range=(bb, be))
     assert torch.equal(out, out_full)
+    # interleaved multi-GPU split (kitc_eval_part): the parts together are bitwise the full run
+    for k in (2, 3, 8):
+        outp = torch.zeros_like(out_full)
+        for r in range(k):
+            G.eval(0, 6, 0.7, 0.01, parts, out=outp, part=(r, k))
+        assert torch.equal(outp, out_full)
     # run-to-run determinism
     G2 = K.Tree(dev(X), 400)
     assert torch.equal(G2.eval(0, 6, 0.7, 0.01, G2.modified_weights(0, 6, dev(W))), out_full)
