@@ -33,6 +33,9 @@ namespace {
 #ifndef KITC_EVAL_MINB1
 #define KITC_EVAL_MINB1 4  // rotlet / combined (measured: 4 beats 5 and 6 on C4)
 #endif
+#ifndef KITC_NEAR_U
+#define KITC_NEAR_U 4  // near field: sources per lane per unrolled iteration (loads hoisted)
+#endif
 #ifndef KITC_NEAR_TEAMS
 #define KITC_NEAR_TEAMS 1  // near field: idle target groups join the participating ones
 #endif
@@ -405,7 +408,7 @@ template <int KER>
 __device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e, int rk, int TS,
                                            const EvalArgs& a, double* acc) {
     using K = EvalKern<KER>;
-    constexpr int M = K::M, U = 4;
+    constexpr int M = K::M, U = KITC_NEAR_U;
     const int self = a.self_omit ? t : -1;
     int j = b + rk;
     for (; j + (U - 1) * TS < e; j += U * TS) {

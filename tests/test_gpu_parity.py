@@ -233,3 +233,18 @@ def test_C3_full_size_sampled(K):
     assert O.rel_error(dref, dgot[tg2]) <= DIRECT_GATE
     E = O.rel_error(dgot, got)
     assert 1e-9 < E < 1e-4
+
+
+def test_batch_targets_prefix(K):
+    # kitc_batch_targets(b) = targets in batches [0, b): batches tile the sorted positions leaf by leaf
+    X, W = KI.particles(7001, seed=8)
+    G = K.Tree(dev(X), 90)
+    nb = G.nbatches
+    pre = np.array([G.batch_targets(b) for b in range(nb + 1)])
+    assert pre[0] == 0 and pre[-1] == 7001
+    d = np.diff(pre)
+    assert d.min() >= 1 and d.max() <= 4
+    fh = G.modified_weights(0, 3, dev(W))
+    b0, b1 = nb // 3, 2 * nb // 3
+    _, st = G.eval(0, 3, 0.7, 0.01, fh, batch_range=(b0, b1), stats=True)
+    assert int((host(st)[:, 4] > 0).sum()) == pre[b1] - pre[b0]
