@@ -183,7 +183,7 @@ kitc_status kitc_rel_error(const double* ref, const double* ap, int64_t n, doubl
 void kitc_tree_free(kitc_tree* t) {
     if (!t) return;
     cudaStream_t s = t->stream;
-    for (DevBuf* b : {&t->x, &t->y, &t->z, &t->perm, &t->x2, &t->y2, &t->z2, &t->perm2, &t->w, &t->box, &t->cr,
+    for (DevBuf* b : {&t->x, &t->y, &t->z, &t->perm, &t->x2, &t->y2, &t->z2, &t->perm2, &t->w, &t->src, &t->box, &t->cr,
                       &t->topo, &t->grid, &t->tord, &t->leaves, &t->bstart, &t->bcount, &t->d_items, &t->d_part, &t->d_cnt, &t->d_off,
                       &t->d_lvl, &t->d_split, &t->d_flag, &t->d_witems, &t->d_wpart, &t->d_tkey, &t->d_tkey2,
                       &t->d_tidx, &t->d_tidx2, &t->d_txyz, &t->d_tcub, &t->d_tbox})

@@ -36,6 +36,9 @@ namespace {
 #ifndef KITC_NEAR_U
 #define KITC_NEAR_U 4  // near field: sources per lane per unrolled iteration (loads hoisted)
 #endif
+#ifndef KITC_NEAR_PACKED
+#define KITC_NEAR_PACKED 1  // near field reads the packed (x, y, z, w) records
+#endif
 #ifndef KITC_NEAR_TEAMS
 #define KITC_NEAR_TEAMS 1  // near field: idle target groups join the participating ones
 #endif
@@ -67,6 +70,8 @@ struct EvalArgs {
     const int* perm;  // output row of target position t
     const int* tord;  // batch slot -> target position (nullptr: identity)
     const double* w;  // sorted weights, M planes of N
+    const double* src;  // packed near-field records (x, y, z, w.., pad), sld doubles each
+    int sld;
     const double4* cr;
     const int4* topo;
     const double* grid;
@@ -416,11 +421,27 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int jj = j + u * TS;
-            sx[u] = __ldg(a.x + jj);
-            sy[u] = __ldg(a.y + jj);
-            sz[u] = __ldg(a.z + jj);
+            if (KITC_NEAR_PACKED) {  // one record: (x, y) (z, w0) (w1, w2) ... 16-byte loads
+                const double2* r = reinterpret_cast<const double2*>(a.src + (size_t)jj * a.sld);
+                double v[((3 + M + 1) / 2) * 2];
 #pragma unroll
-            for (int m = 0; m < M; ++m) f[u][m] = __ldg(a.w + (size_t)m * a.N + jj);
+                for (int q = 0; q < (3 + M + 1) / 2; ++q) {
+                    const double2 d2 = __ldg(r + q);
+                    v[2 * q] = d2.x;
+                    v[2 * q + 1] = d2.y;
+                }
+                sx[u] = v[0];
+                sy[u] = v[1];
+                sz[u] = v[2];
+#pragma unroll
+                for (int m = 0; m < M; ++m) f[u][m] = v[3 + m];
+            } else {
+                sx[u] = __ldg(a.x + jj);
+                sy[u] = __ldg(a.y + jj);
+                sz[u] = __ldg(a.z + jj);
+#pragma unroll
+                for (int m = 0; m < M; ++m) f[u][m] = __ldg(a.w + (size_t)m * a.N + jj);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -702,6 +723,8 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     a.ty = a.y;
     a.tz = a.z;
     a.w = t->w.as<double>();
+    a.src = t->src.as<double>();
+    a.sld = t->src_ld;
     a.cr = t->cr.as<double4>();
     a.topo = t->topo.as<int4>();
     a.grid = t->grid.as<double>();

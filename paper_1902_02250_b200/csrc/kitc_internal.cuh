@@ -74,6 +74,8 @@ struct kitc_tree {
     kitc::DevBuf x2, y2, z2, perm2;      // partition scratch
     kitc::DevBuf w;                      // sorted weights, m planes of N doubles
     int32_t w_m = 0;
+    kitc::DevBuf src;                    // packed near-field records (x, y, z, w.., pad), src_ld doubles each
+    int32_t src_ld = 0;
     bool weights_ready = false;
     int32_t grid_n = -1;                 // degree of the stored grids
     int32_t weights_kernel = -1;

@@ -47,12 +47,25 @@ struct Peers {
     int n;
 };
 
+// ws[c][i] = w[perm[i]][c] (SoA planes, Algorithm 1) and the packed near-field
+// source records src[i] = (x, y, z, w_0 .. w_{m-1}, 0 pad) of sld doubles (16-B
+// multiple), read by k_eval's near field with 16-byte loads.
 __global__ void k_gather_w(const double* __restrict__ w, const int* __restrict__ perm, int N, int m,
-                           double* __restrict__ ws) {
+                           double* __restrict__ ws, const double* __restrict__ x, const double* __restrict__ y,
+                           const double* __restrict__ z, int sld, double* __restrict__ src) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const size_t o = (size_t)perm[i] * m;
-    for (int c = 0; c < m; ++c) ws[(size_t)c * N + i] = w[o + c];
+    double* r = src + (size_t)i * sld;
+    r[0] = x[i];
+    r[1] = y[i];
+    r[2] = z[i];
+    for (int c = 0; c < m; ++c) {
+        const double v = w[o + c];
+        ws[(size_t)c * N + i] = v;
+        r[3 + c] = v;
+    }
+    for (int c = 3 + m; c < sld; ++c) r[c] = 0.0;
 }
 
 // grid s_{l,k} = c_l + h_l t_k, s_{l,0} = hi_l, s_{l,n} = lo_l (reading A13), RN.
@@ -217,7 +230,12 @@ kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, i
     const long long LEN = fhat_cluster_len(P, m);
     // sorted weights (SoA, m planes)
     KITC_TRY(t->w.ensure((size_t)m * N * sizeof(double), s));
-    k_gather_w<<<(N + 255) / 256, 256, 0, s>>>(w, t->perm.as<int>(), N, m, t->w.as<double>()); note_launch();
+    const int sld = (3 + m + 1) & ~1;
+    KITC_TRY(t->src.ensure((size_t)N * sld * sizeof(double), s));
+    t->src_ld = sld;
+    k_gather_w<<<(N + 255) / 256, 256, 0, s>>>(w, t->perm.as<int>(), N, m, t->w.as<double>(), t->x.as<double>(),
+                                               t->y.as<double>(), t->z.as<double>(), sld, t->src.as<double>());
+    note_launch();
     // grids of every cluster (reading A12: t_k = sin(pi (n - 2k) / (2n)))
     Nodes nd;
     for (int k = 0; k <= n; ++k) nd.t[k] = std::sin(kPi * (double)(n - 2 * k) / (2.0 * (double)n));
