@@ -355,7 +355,9 @@ def run_kitc(args, cfg, rank, world, local_rank):
     line = {"metric": metric_for(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": f"synthetic (kitc_inputs: {cfg['geometry']}, weights uniform [-1,1]^m, seed 0)",
+            "data": "synthetic (kitc_inputs: " + (
+                "organism pairs of the paper's Example 1, unit forces +-t" if cfg["geometry"] == "organisms"
+                else f"{cfg['geometry']}, weights uniform [-1,1]^m") + ", seed 0)",
             "config": {"workload": f"{args.config} ({KI.CONFIGS[args.config]})",
                        "parallelism": f"tree replicated, fhat sharded, targets dp{world} (64-batch chunks interleaved)",
                        "fhat_exchange": exchange,

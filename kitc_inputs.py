@@ -14,8 +14,13 @@ Recipe (BASELINE.json configs):
            points on a centred square grid of spacing 16/15 (s = 15 spans [-8, 8]^2,
            constant density as s grows); positions are deterministic, then
            W = rng.uniform(-1, 1, (N, m)) (force and torque components in [-1, 1]).
+  organisms: the paper's Example 1: N/2 microorganisms, each a body at
+           b = rng.uniform(0, 10, 3) and a flagellum at b + 0.02 t (t = a normalised standard
+           normal 3-vector), carrying the unit forces +t and -t ("unit forces in opposite
+           directions along the organism length"); bodies first, then directions, drawn per
+           organism in one call each; particle 2i = body i, 2i+1 = flagellum i.
 The uniform cube stands in for the paper's Example 1 (random organisms in a
-cube); the sphere surface stands in for the non-uniform,
+cube), which "organisms" reproduces; the sphere surface stands in for the non-uniform,
 flat-box geometry of Example 2, which "rods" reproduces.
 """
 from __future__ import annotations
@@ -32,7 +37,12 @@ CONFIGS = {
     # not a BASELINE config: the paper's own Example 2 parallel run (Table 5):
     # 80^2 rods x 151 points, Stokeslet + rotlet, eps = 0.3, theta = 0.7, n = 7, N0 = 1000
     "X2": dict(N=966_400, geometry="rods", kernel=2, eps=0.3, n=7, theta=0.7, N0=1000),
+    # not BASELINE configs: the paper's Example 1 rows of Table 1:
+    # organism pairs in a side-10 cube, Stokeslet, eps = 0.02, theta = 0.7, n = 7, N0 = 2000
+    "X1": dict(N=640_000, geometry="organisms", kernel=0, eps=0.02, n=7, theta=0.7, N0=2000),
+    "X1L": dict(N=5_120_000, geometry="organisms", kernel=0, eps=0.02, n=7, theta=0.7, N0=2000),
 }
+ORG_L, ORG_ELL = 10.0, 0.02   # cube side and organism length
 ROD_M = 150          # segments per rod
 ROD_SPACING = 16.0 / 15.0
 
@@ -62,6 +72,21 @@ def particles(N: int, geometry: str = "uniform", seed: int = 0, m: int = 3):
         if side * side * (ROD_M + 1) != N:
             raise ValueError(f"rods: N must be s^2 x {ROD_M + 1}")
         X = rod_positions(side)
+    elif geometry == "organisms":
+        if N % 2:
+            raise ValueError("organisms: N must be even (body + flagellum pairs)")
+        B = rng.uniform(0.0, ORG_L, (N // 2, 3))
+        G = rng.standard_normal((N // 2, 3))
+        T = G / np.linalg.norm(G, axis=1, keepdims=True)
+        X = np.empty((N, 3))
+        X[0::2] = B
+        X[1::2] = B + ORG_ELL * T
+        if m != 3:
+            raise ValueError("organisms: Stokeslet forces (m = 3)")
+        W = np.empty((N, 3))
+        W[0::2] = T
+        W[1::2] = -T
+        return np.ascontiguousarray(X), np.ascontiguousarray(W)
     elif geometry == "slab":
         # thin slab (extents 2 x 2 x 0.25): exercises 4-way splits
         X = rng.uniform(-1.0, 1.0, (N, 3)) * np.array([1.0, 1.0, 0.125])

@@ -116,3 +116,15 @@ def test_binding_declares_every_signature():
         m = re.search(r"\b" + name + r"\s*\(([^)]*)\)", src)
         params = [p for p in m.group(1).split(",") if p.strip() and p.strip() != "void"]
         assert len(params) == len(args), name
+
+
+def test_organisms_generator_matches_paper_example1():
+    # pairs (body, flagellum) at distance 0.02 in a side-10 cube, unit forces +-t
+    import numpy as np
+    import kitc_inputs as KI
+    X, W = KI.particles(10000, "organisms", seed=3)
+    d = X[1::2] - X[0::2]
+    assert np.allclose(np.linalg.norm(d, axis=1), 0.02, rtol=1e-12)
+    assert np.allclose(W[0::2], d / 0.02, atol=1e-12) and np.array_equal(W[1::2], -W[0::2])
+    assert X[0::2].min() >= 0 and X[0::2].max() <= 10
+    assert KI.CONFIGS["X1"]["N"] == 640_000 and KI.CONFIGS["X1L"]["N"] == 5_120_000   # Table 1 rows

@@ -74,7 +74,8 @@ def assert_same_tree(T, G):
 
 @pytest.mark.parametrize("N,N0,geom", [(1000, 100, "uniform"), (100_000, 500, "uniform"),
                                        (50_000, 64, "sphere"), (20_000, 40, "slab"),
-                                       (5000, 1, "uniform"), (33, 100, "uniform"), (5436, 40, "rods")])
+                                       (5000, 1, "uniform"), (33, 100, "uniform"), (5436, 40, "rods"),
+                                       (20000, 100, "organisms")])
 def test_tree_bit_exact(K, N, N0, geom):
     X, _ = KI.particles(N, geom, seed=7)
     T = O.Tree(X, N0)
@@ -134,6 +135,7 @@ def run_gpu(K, X, W, kern, n, theta, N0, eps, self_omit=True):
     (1001, 19, 7, 0.7, 1, 0.02, "sphere"),        # odd N, rotlet, partial last fhat block
     (3, 1, 1, 0.7, 0, 0.01, "uniform"),           # tiny: one-particle leaves
     (3775, 100, 7, 0.7, 2, 0.3, "rods"),          # paper Example 2 geometry (5^2 rods), Stokeslet + rotlet
+    (12000, 300, 7, 0.7, 0, 0.02, "organisms"),   # paper Example 1 geometry (organism pairs)
 ])
 def test_treecode_parity(K, N, N0, n, theta, kern, eps, geom):
     m = O.DIMS[kern][0]
