@@ -406,15 +406,15 @@ __device__ __forceinline__ void far_field_team(double x, double y, double z, con
 }
 
 // Near field of one rejected leaf: the lane of rank `rk` in a team of TS lanes
-// working for target t (position x, y, z) sums sources b + rk, b + rk + TS, ...
-// (unrolled x4 with the loads hoisted).  The self pair (j == t under SELF_OMIT)
-// is evaluated with f = 0 and s = 1: an exact zero contribution, no branch.
-template <int KER>
-__device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e, int rk, int TS,
-                                           const EvalArgs& a, double* acc) {
+// working for a target at (x, y, z) sums sources b + rk, b + rk + TS, ...
+// (unrolled x4 with the loads hoisted).  SELF: the target is source `self` of
+// this leaf, whose pair is evaluated with f = 0 and s = 1 -- an exact zero
+// contribution, no branch.
+template <int KER, bool SELF>
+__device__ __forceinline__ void near_field_impl(double x, double y, double z, int self, int b, int e, int rk, int TS,
+                                                const EvalArgs& a, double* acc) {
     using K = EvalKern<KER>;
     constexpr int M = K::M, U = KITC_NEAR_U;
-    const int self = a.self_omit ? t : -1;
     int j = b + rk;
     for (; j + (U - 1) * TS < e; j += U * TS) {
         double sx[U], sy[U], sz[U], f[U][M];
@@ -445,16 +445,18 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const bool me = (j + u * TS) == self;
+            const bool me = SELF && (j + u * TS) == self;
             const double dx = x - sx[u], dy = y - sy[u], dz = z - sz[u];
+            if (SELF) {
 #pragma unroll
-            for (int m = 0; m < M; ++m) f[u][m] = me ? 0.0 : f[u][m];
+                for (int m = 0; m < M; ++m) f[u][m] = me ? 0.0 : f[u][m];
+            }
             const double s = me ? 1.0 : fma(dx, dx, fma(dy, dy, fma(dz, dz, a.kp.e2)));
             K::pair(dx, dy, dz, s, f[u], acc, a.kp);
         }
     }
     for (; j < e; j += TS) {
-        const bool me = j == self;
+        const bool me = SELF && j == self;
         const double dx = x - __ldg(a.x + j), dy = y - __ldg(a.y + j), dz = z - __ldg(a.z + j);
         double f[M];
 #pragma unroll
@@ -462,6 +464,17 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
         const double s = me ? 1.0 : fma(dx, dx, fma(dy, dy, fma(dz, dz, a.kp.e2)));
         K::pair(dx, dy, dz, s, f, acc, a.kp);
     }
+}
+
+// The self pair can only occur in the leaf holding the target; every other leaf
+// runs the select-free loop (warp-uniform: a batch never straddles leaves).
+template <int KER>
+__device__ __forceinline__ void near_field(double x, double y, double z, int t, int b, int e, int rk, int TS,
+                                           const EvalArgs& a, double* acc) {
+    if (a.self_omit && t >= b && t < e)
+        near_field_impl<KER, true>(x, y, z, t, b, e, rk, TS, a, acc);
+    else
+        near_field_impl<KER, false>(x, y, z, -1, b, e, rk, TS, a, acc);
 }
 
 // Near field of leaf [b, e) for the participating lanes `rm` (whole target groups).
