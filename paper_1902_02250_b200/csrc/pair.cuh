@@ -10,6 +10,9 @@
 // (substitute r^2 = s - eps^2).  Constants 1/(8 pi), 1/2, 1/4 are applied once
 // per target at the end (scale()).  These differ from the literal formulas by
 // rounding only.
+//   Kern<KER>      pair terms with s^{-1/2} to ~4 ulp: the direct sum (kitc_direct)
+//   EvalKern<KER>  treecode-evaluation forms (row form for the far field, scaled
+//                  accumulators, one-step Newton s^{-1/2}: reading A19)
 #pragma once
 #include <cuda_runtime.h>
 
@@ -71,29 +74,6 @@ template <> struct Kern<0> {
         acc[1] = fma(c, dy, fma(f[1], h1, acc[1]));
         acc[2] = fma(c, dz, fma(f[2], h1, acc[2]));
     }
-    // Far-field row form: along one proxy row (k1, k2) dx and dy are fixed, so
-    // sum_k3 c_k d_k = (dx C, dy C, Z) with C = sum c_k, Z = sum c_k dz_k:
-    // 2 instead of 3 FMAs per pair for the [f.d] d H2 term.
-    struct Row {
-        double C = 0.0, Z = 0.0;
-    };
-    static __device__ __forceinline__ void pair_row(double dx, double dy, double dz, double rs, const double* f,
-                                                    double* acc, Row& r, const KParams& k) {
-        double rs2 = rs * rs;
-        double rs3 = rs2 * rs;
-        double h1 = fma(k.e2, rs3, rs);
-        double c = fma(f[0], dx, fma(f[1], dy, f[2] * dz)) * rs3;
-        r.C += c;
-        r.Z = fma(c, dz, r.Z);
-        acc[0] = fma(f[0], h1, acc[0]);
-        acc[1] = fma(f[1], h1, acc[1]);
-        acc[2] = fma(f[2], h1, acc[2]);
-    }
-    static __device__ __forceinline__ void row_end(double dx, double dy, const Row& r, double* acc) {
-        acc[0] = fma(r.C, dx, acc[0]);
-        acc[1] = fma(r.C, dy, acc[1]);
-        acc[2] += r.Z;
-    }
     // 1/(8 pi)
     static __device__ __forceinline__ double scale(int) { return 1.0 / (8.0 * 3.14159265358979323846); }
 };
@@ -125,42 +105,6 @@ template <> struct Kern<1> {
         acc[3] = fma(gd, dx, fma(g[0], d1, acc[3]));
         acc[4] = fma(gd, dy, fma(g[1], d1, acc[4]));
         acc[5] = fma(gd, dz, fma(g[2], d1, acc[5]));
-    }
-    // Far-field row form (dx, dy fixed along a row):
-    //   sum Q (g x d) = (B1 - dy A2, dx A2 - B0, dy A0 - dx A1), A = sum Q g, B = sum Q dz g
-    //   sum (g.d) D2 d = (dx T, dy T, TZ),  T = sum (g.d) D2, TZ = sum (g.d) D2 dz
-    struct Row {
-        double A0 = 0.0, A1 = 0.0, A2 = 0.0, B0 = 0.0, B1 = 0.0, T = 0.0, TZ = 0.0;
-    };
-    static __device__ __forceinline__ void pair_row(double dx, double dy, double dz, double rs, const double* g,
-                                                    double* acc, Row& r, const KParams& k) {
-        double rs2 = rs * rs;
-        double rs3 = rs2 * rs;
-        double rs5 = rs3 * rs2;
-        double rs7 = rs5 * rs2;
-        double q = fma(k.e2x3, rs5, 2.0 * rs3);
-        double d1 = fma(k.e4x15, rs7, -q);
-        double d2 = fma(k.e2x15, rs7, 6.0 * rs5);
-        r.A0 = fma(q, g[0], r.A0);
-        r.A1 = fma(q, g[1], r.A1);
-        r.A2 = fma(q, g[2], r.A2);
-        double qz = q * dz;
-        r.B0 = fma(qz, g[0], r.B0);
-        r.B1 = fma(qz, g[1], r.B1);
-        acc[3] = fma(g[0], d1, acc[3]);
-        acc[4] = fma(g[1], d1, acc[4]);
-        acc[5] = fma(g[2], d1, acc[5]);
-        double t = fma(g[0], dx, fma(g[1], dy, g[2] * dz)) * d2;
-        r.T += t;
-        r.TZ = fma(t, dz, r.TZ);
-    }
-    static __device__ __forceinline__ void row_end(double dx, double dy, const Row& r, double* acc) {
-        acc[0] += fma(-dy, r.A2, r.B1);
-        acc[1] += fma(dx, r.A2, -r.B0);
-        acc[2] += fma(dy, r.A0, -dx * r.A1);
-        acc[3] = fma(r.T, dx, acc[3]);
-        acc[4] = fma(r.T, dy, acc[4]);
-        acc[5] += r.TZ;
     }
     // u: 1/(16 pi), w: 1/(32 pi)
     static __device__ __forceinline__ double scale(int c) {
@@ -200,36 +144,10 @@ template <> struct Kern<2> {
         acc[4] = fma(fy, q2, fma(gd, dy, fma(g[1], d1, acc[4])));
         acc[5] = fma(fz, q2, fma(gd, dz, fma(g[2], d1, acc[5])));
     }
-    // far-field row form: plain pair (not the benchmark kernel)
-    struct Row {};
-    static __device__ __forceinline__ void pair_row(double dx, double dy, double dz, double rs, const double* f,
-                                                    double* acc, Row&, const KParams& k) {
-        pair_rs(dx, dy, dz, rs, f, acc, k);
-    }
-    static __device__ __forceinline__ void row_end(double, double, const Row&, double*) {}
     static __device__ __forceinline__ double scale(int c) {
         return c < 3 ? 1.0 / (16.0 * 3.14159265358979323846) : 1.0 / (32.0 * 3.14159265358979323846);
     }
 };
-
-// KC independent pairs evaluated stage by stage, each into its own accumulator
-// set acc[i]: the s^{-1/2} refinement chains of the KC pairs are interleaved so
-// the FP64 pipe sees KC independent instructions per warp (it needs ~4 to
-// saturate: profiles/r01_fp64_lat.txt).
-template <int KER, int KC>
-__device__ __forceinline__ void pairs(const double* dx, const double* dy, const double* dz, const double* s,
-                                      const double (*f)[Kern<KER>::M], double (*acc)[Kern<KER>::P],
-                                      const KParams& k) {
-    double y[KC], e[KC], rs[KC];
-#pragma unroll
-    for (int i = 0; i < KC; ++i) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[i]) : "d"(s[i]));
-#pragma unroll
-    for (int i = 0; i < KC; ++i) e[i] = fma(-(s[i] * y[i]), y[i], 1.0);
-#pragma unroll
-    for (int i = 0; i < KC; ++i) rs[i] = fma(y[i] * e[i], fma(0.375, e[i], 0.5), y[i]);
-#pragma unroll
-    for (int i = 0; i < KC; ++i) Kern<KER>::pair_rs(dx[i], dy[i], dz[i], rs[i], f[i], acc[i], k);
-}
 
 inline KParams make_kparams(double eps) {
     KParams k;
@@ -248,27 +166,10 @@ inline KParams make_kparams(double eps) {
 // ---------------------------------------------------------------------------
 // Treecode-evaluation forms (eval.cu).  EvalKern<KER> exposes
 //   NA accumulators, pair(dx,dy,dz,s,f,acc), pair_row(dx,dy,dz,s,f,acc,row),
-//   row_end(dx,dy,row,acc), out(acc,c) -> output component c (scaled)
-// taking s = |d|^2 + eps^2 (not its rsqrt).  The rotlet and combined kernels use
-// the Kern<> forms above; the Stokeslet has its own cheaper form.
-template <int KER> struct EvalKern {
-    using K = Kern<KER>;
-    static constexpr int M = K::M, P = K::P, NA = K::P;
-    static constexpr bool kPairRows = true;  // far field: two rows per lane (register budget permitting)
-    using Row = typename K::Row;
-    static __device__ __forceinline__ void pair(double dx, double dy, double dz, double s, const double* f,
-                                                double* acc, const KParams& k) {
-        K::pair(dx, dy, dz, s, f, acc, k);
-    }
-    static __device__ __forceinline__ void pair_row(double dx, double dy, double dz, double s, const double* f,
-                                                    double* acc, Row& r, const KParams& k) {
-        K::pair_row(dx, dy, dz, rsqrt_fast(s), f, acc, r, k);
-    }
-    static __device__ __forceinline__ void row_end(double dx, double dy, const Row& r, double* acc) {
-        K::row_end(dx, dy, r, acc);
-    }
-    static __device__ __forceinline__ double out(const double* acc, int c) { return acc[c] * K::scale(c); }
-};
+//   row_end(dx,dy,row,acc), out(acc,c) -> output component c (scaled),
+//   kPairRows (far field: two rows per lane),
+// taking s = |d|^2 + eps^2; all three kernels use Y = 2 s^{-1/2} (rsqrt2_newton).
+template <int KER> struct EvalKern;
 
 // Stokeslet with Y = 2 s^{-1/2} (rsqrt2_newton): 16 pi H1 = 2 rs + 2 eps^2 rs^3 =
 // Y + (eps^2/4) Y^3 and 16 pi H2 = 2 rs^3 = Y^3 / 4, so
