@@ -28,7 +28,7 @@ namespace {
 #define KITC_EVAL_WARPS 4
 #endif
 #ifndef KITC_EVAL_MINB
-#define KITC_EVAL_MINB 4  // resident CTAs per SM (register budget), Stokeslet (measured: 4 > 5 > 6, 3)
+#define KITC_EVAL_MINB 5  // resident CTAs per SM (register budget), Stokeslet (measured: 5 > 4 > 6 with dz in smem)
 #endif
 #ifndef KITC_EVAL_MINB1
 #define KITC_EVAL_MINB1 4  // rotlet / combined (measured: 4 beats 5 and 6 on C4)
@@ -44,6 +44,9 @@ namespace {
 #endif
 #ifndef KITC_FAR_TEAMS
 #define KITC_FAR_TEAMS 1  // far field: idle target groups join 1 or 2 accepting targets
+#endif
+#ifndef KITC_DZ_SMEM
+#define KITC_DZ_SMEM 1  // far field: per-plane dz of the batch's targets in shared memory
 #endif
 #ifndef KITC_EVAL_SB
 #define KITC_EVAL_SB 2
@@ -97,6 +100,7 @@ struct EvalArgs {
 // mbarriers, the number of rounds issued so far (-> buffer and phase parity of
 // the next round), and the DFS stack.
 struct WarpSmem {
+    double* dzs;               // kBatch x P doubles (KITC_DZ_SMEM)
     double* buf;               // 2 x blk doubles
     unsigned long long* bar;   // 2 mbarriers
     int* nround;
@@ -161,11 +165,18 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
         issue(0, base);
         if (NS > 1) issue(1, base + 1);
     }
+#if KITC_DZ_SMEM
+    // dz per plane of this lane's target, in shared memory (frees registers)
+    double* dz = ws.dzs + (lane / kGroup) * P;
+    for (int k3 = grp; k3 < P; k3 += kGroup) dz[k3] = z - __ldg(g + 2 * P + k3);
+    __syncwarp(am);
+#else
     double dz[PT > 0 ? PT : 1];
     if constexpr (PT > 0) {
 #pragma unroll
         for (int k3 = 0; k3 < PT; ++k3) dz[k3] = z - __ldg(g + 2 * PT + k3);
     }
+#endif
     for (int st = 0; st < NS; ++st) {
         const int k = base + st;
         const double* B = ws.buf + (k & 1) * kSB * blk;
@@ -552,7 +563,8 @@ __global__ void __launch_bounds__(kWarps * 32, KER == 0 ? KITC_EVAL_MINB : KITC_
         ws.buf = reinterpret_cast<double*>(base);
         ws.bar = reinterpret_cast<unsigned long long*>(base + 2 * kSB * blk * sizeof(double));
         ws.nround = reinterpret_cast<int*>(ws.bar + 2);
-        ws.stk = reinterpret_cast<int2*>(ws.bar + 3);
+        ws.dzs = reinterpret_cast<double*>(ws.bar + 3);
+        ws.stk = reinterpret_cast<int2*>(ws.dzs + (KITC_DZ_SMEM ? kBatch * P : 0));
         if (lane == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(ws.bar)));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(ws.bar + 1)));
@@ -773,6 +785,7 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     if (reinterpret_cast<uintptr_t>(fhat) % 16) return set_error(KITC_EINVAL, "kitc_eval: fhat must be 16-byte aligned");
     // per warp: 2 stage buffers + 2 mbarriers + round counter (8 B) + stack, 128-B multiple
     a.warp_smem = (int)(((size_t)2 * kSB * (n + 1) * m * kRows * sizeof(double) + 24 + (size_t)a.stack_cap * sizeof(int2) +
+                         (KITC_DZ_SMEM ? (size_t)kBatch * (n + 1) * sizeof(double) : 0) +
                          127) / 128 * 128);
     const size_t smem = (size_t)kWarps * a.warp_smem;
     if (smem > 200 * 1024) return set_error(KITC_EINVAL, "kitc_eval: tree too deep for the traversal stack");
