@@ -1,20 +1,25 @@
 // eval.cu -- treecode evaluation (Algorithm 2 lines 7-17) on sm_100a.
 //
-// One warp = one batch of <= kBatch targets of one leaf, consecutive in the
-// leaf's Morton order (spatially compact); kGroup lanes cooperate on each
-// target (they split its proxies / sources and combine at the end).  The warp walks the tree depth-first with an explicit
-// shared-memory stack of (cluster, lane mask) entries, so every lane keeps the
-// paper's PER-TARGET semantics: a lane stops descending below a cluster it
-// accepted; lanes that reject a cluster descend into its children.  At each
-// popped cluster:
+// One warp = one batch of <= kBatch = 4 targets of one leaf, consecutive in the
+// leaf's Morton order (spatially compact); kGroup = 8 lanes cooperate on each
+// target (they split its proxy rows / sources and combine at the end).  The warp
+// walks the tree depth-first with an explicit shared-memory stack of (cluster,
+// lane mask) entries, so every lane keeps the paper's PER-TARGET semantics: a
+// lane stops descending below a cluster it accepted; lanes that reject a cluster
+// descend into its children.  At each popped cluster:
 //   MAC   r^2 <= (theta^2) R^2, R^2 > 0   (RN intrinsics, no FMA; readings A4/A5)
-//   far   accepted lanes sum the kernel against the (n+1)^3 proxies s_k with the
-//         modified weights fhat_k (Eq. pc_approximation_3D);
-//         uniform (broadcast) loads of fhat, tensor-product reuse of dx, dy, dz
+//   far   accepting lanes sum the kernel against the (n+1)^3 proxies s_k with the
+//         modified weights fhat_k (Eq. pc_approximation_3D): fhat
+//         staged into shared memory by cp.async.bulk (TMA) two stages ahead,
+//         tensor-product reuse of dx, dy, dz, two rows per lane (far_field); a
+//         cluster accepted by only 1 or 2 targets is done by the whole warp
+//         (far_field_team)
 //   near  rejecting lanes at a leaf sum over its particles directly
-//         (Eq. pc_interaction_3D), j == i skipped by index (reading A8)
+//         (Eq. pc_interaction_3D), j == i skipped by index (reading A8); idle
+//         target groups join 1 or 2 participating targets (near_leaf)
 //   else  rejecting lanes push the children.
 // Outputs are scaled once and scattered to original order (out[perm[t]]).
+// DESIGN.md §6 has the measured effect of each choice.
 #include <algorithm>
 
 #include "kitc_internal.cuh"
@@ -96,9 +101,9 @@ struct EvalArgs {
     KParams kp;
 };
 
-// ---- per-warp shared memory: two fhat round buffers (TMA destinations), their
-// mbarriers, the number of rounds issued so far (-> buffer and phase parity of
-// the next round), and the DFS stack.
+// ---- per-warp shared memory: two fhat stage buffers (TMA destinations), their
+// mbarriers, the number of stages issued so far (-> buffer and phase parity of
+// the next stage), the per-plane dz of the batch's targets, and the DFS stack.
 struct WarpSmem {
     double* dzs;               // kBatch x P doubles (KITC_DZ_SMEM)
     double* buf;               // 2 x blk doubles

@@ -136,6 +136,9 @@ def run_gpu(K, X, W, kern, n, theta, N0, eps, self_omit=True):
     (3, 1, 1, 0.7, 0, 0.01, "uniform"),           # tiny: one-particle leaves
     (3775, 100, 7, 0.7, 2, 0.3, "rods"),          # paper Example 2 geometry (5^2 rods), Stokeslet + rotlet
     (12000, 300, 7, 0.7, 0, 0.02, "organisms"),   # paper Example 1 geometry (organism pairs)
+    (4000, 100, 5, 0.7, 0, 0.0, "uniform"),       # eps = 0: the singular (classical) Stokeslet
+    (1500, 40, 16, 0.7, 1, 0.01, "uniform"),      # maximum degree n = 16 (runtime-P kernel), rotlet
+    (2500, 80, 6, 0.95, 2, 0.02, "slab"),         # theta close to 1, combined kernel, 4-way splits
 ])
 def test_treecode_parity(K, N, N0, n, theta, kern, eps, geom):
     m = O.DIMS[kern][0]
