@@ -13,7 +13,8 @@
 // k_eval stages one round with one bulk copy; padding rows of the last round are 0.
 // Chunks of one cluster write partials that a second kernel sums in chunk
 // order (deterministic).  Reading A15: L per axis instead of
-// (a1 a2 a3 / denom) -- rounding-only difference.
+// (a1 a2 a3 / denom), reciprocals by Newton-refined MUFU seeds -- rounding-only
+// differences (parity gate 1e-13 per cluster).
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -83,31 +84,35 @@ __global__ void k_grids(int C, int n, Nodes nd, const double* __restrict__ box, 
     }
 }
 
+// 1/d for normal |d| (> DBL_MIN here): MUFU seed + two Newton steps (~1 ulp), no
+// IEEE-division slow path (its branch serialises the warp).
+__device__ __forceinline__ double rcp_nr(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-d, y, 1.0);
+    return fma(y, e, y);
+}
+
 // 1D barycentric vector of coordinate v on nodes s (Algorithm 1 lines 9-17).
 template <int P>
 __device__ __forceinline__ void bary(double v, const double* s, double* L) {
     double sum = 0.0;
     int flag = -1;
+    double a[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) {
         const double diff = v - s[k];
         const double wk = (k == 0 || k == P - 1) ? ((k & 1) ? -0.5 : 0.5) : ((k & 1) ? -1.0 : 1.0);
-        if (fabs(diff) <= DBL_MIN) {
-            flag = k;
-            L[k] = 0.0;
-        } else {
-            L[k] = wk / diff;
-            sum += L[k];
-        }
+        const bool hit = fabs(diff) <= DBL_MIN;
+        flag = hit ? k : flag;
+        a[k] = hit ? 0.0 : wk * rcp_nr(hit ? 1.0 : diff);
+        sum += a[k];
     }
-    if (flag >= 0) {
+    const double inv = rcp_nr(flag >= 0 ? 1.0 : sum);
 #pragma unroll
-        for (int k = 0; k < P; ++k) L[k] = (k == flag) ? 1.0 : 0.0;
-    } else {
-        const double inv = 1.0 / sum;
-#pragma unroll
-        for (int k = 0; k < P; ++k) L[k] *= inv;
-    }
+    for (int k = 0; k < P; ++k) L[k] = flag >= 0 ? (k == flag ? 1.0 : 0.0) : a[k] * inv;
 }
 
 template <int P, int M>
@@ -132,13 +137,16 @@ __global__ void __launch_bounds__((P * P + 31) / 32 * 32) k_weights(
     __syncthreads();
     for (int tile = it.b; tile < it.e; tile += kTile) {
         const int cnt = min(kTile, it.e - tile);
-        for (int j = tid; j < cnt; j += NT) {
-            const int i = tile + j;
-            bary<P>(x[i], sg, Lx[j]);
-            bary<P>(y[i], sg + P, Ly[j]);
-            bary<P>(z[i], sg + 2 * P, Lz[j]);
-#pragma unroll
-            for (int m = 0; m < M; ++m) sw[j][m] = ws[(size_t)m * N + i];
+        // phase 1: the 3 cnt per-axis vectors spread over all threads
+        for (int q = tid; q < 3 * cnt; q += NT) {
+            const int l = q / cnt, j = q - l * cnt, i = tile + j;
+            const double* coord = l == 0 ? x : l == 1 ? y : z;
+            double(*L)[P] = l == 0 ? Lx : l == 1 ? Ly : Lz;
+            bary<P>(coord[i], sg + l * P, L[j]);
+        }
+        for (int q = tid; q < M * cnt; q += NT) {
+            const int m = q / cnt, j = q - m * cnt;
+            sw[j][m] = ws[(size_t)m * N + tile + j];
         }
         __syncthreads();
         if (owner) {
