@@ -3,7 +3,8 @@
  * barycentric Lagrange kernel-independent treecode (KITC) of Wang, Krasny and
  * Tlupova, arXiv:1902.02250.  P:<n> = PAPER.md line n.
  *
- * The library computes, for targets = sources x_i (i = 0..N-1),
+ * The library computes, for targets = sources x_i (i = 0..N-1) -- or for a
+ * separate target set (kitc_eval_targets) --
  *     u(x_i) = sum_j k(x_i, x_j) f_j                       (Eq. N-body)
  * with the particle-cluster treecode of Algorithm 2: a tree of
  * rectangular clusters, modified weights at (n+1)^3 Chebyshev
@@ -32,7 +33,10 @@
  *    CUDA errors observed by the call.
  *  - Everything is fp64.  Results are deterministic: bitwise identical run to
  *    run and independent of how batch / cluster ranges are split across calls
- *    or ranks.
+ *    or ranks (kitc_eval, kitc_eval_ex, kitc_eval_part, the peer-replicated
+ *    modified weights).  The treecode evaluation uses a one-Newton-step
+ *    s^{-1/2} (relative error < 2e-12; reading A19); kitc_direct
+ *    keeps ~4 ulp.
  */
 #ifndef KITC_H
 #define KITC_H
