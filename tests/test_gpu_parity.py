@@ -253,3 +253,43 @@ def test_batch_targets_prefix(K):
     b0, b1 = nb // 3, 2 * nb // 3
     _, st = G.eval(0, 3, 0.7, 0.01, fh, batch_range=(b0, b1), stats=True)
     assert int((host(st)[:, 4] > 0).sum()) == pre[b1] - pre[b0]
+
+
+@pytest.mark.slow
+def test_C4_full_size_sampled(K):
+    # rotlet at the bench size: sampled targets against the oracle treecode on the full tree
+    c = KI.CONFIGS["C4"]
+    X, W = KI.config_particles("C4")
+    tg = KI.sample_targets(c["N"], 120, seed=4)
+    T = O.Tree(X, c["N0"])
+    F = T.modified_weights(W, c["n"])
+    ref, rst = T.treecode(1, c["eps"], c["n"], c["theta"], W, fhat=F, targets=tg, stats=True)
+    got, gst, G = run_gpu(K, X, W, 1, c["n"], c["theta"], c["N0"], c["eps"])
+    assert O.rel_error(ref, got[tg]) <= TREE_GATE
+    assert np.array_equal(rst.astype(np.int64), gst[tg])
+
+
+@pytest.mark.slow
+def test_C5_full_size_properties(K):
+    # 1e7 points on the sphere: tree bit-exact, exact interaction counts on sampled targets (they
+    # depend only on MAC decisions: the oracle runs with zero weights), coverage of every target,
+    # direct sum on sampled targets vs the oracle, treecode error vs the GPU direct sum
+    c = KI.CONFIGS["C5"]
+    X, W = KI.config_particles("C5")
+    T = O.Tree(X, c["N0"])
+    G = K.Tree(dev(X), c["N0"])
+    assert G.nclusters == T.nclusters and G.depth == T.depth
+    assert np.array_equal(G.export()["perm"], T.perm)
+    fh = G.modified_weights(0, c["n"], dev(W))
+    out, st = G.eval(0, c["n"], c["theta"], c["eps"], fh, stats=True)
+    st = host(st)
+    assert np.all(st[:, 4] == c["N"])                       # every source covered exactly once
+    tg = KI.sample_targets(c["N"], 25, seed=5)
+    Z = np.zeros((T.nclusters, 3, (c["n"] + 1) ** 3))
+    _, rst = T.treecode(0, c["eps"], c["n"], c["theta"], W, fhat=Z, targets=tg, stats=True)
+    assert np.array_equal(rst.astype(np.int64), st[tg])
+    dref = O.direct(0, c["eps"], X, W, targets=tg[:8])
+    dgot = host(K.direct_sample(dev(X), dev(W), 0, c["eps"], torch.from_numpy(tg).cuda()))
+    assert O.rel_error(dref, dgot[:8]) <= DIRECT_GATE
+    E = O.rel_error(dgot, host(out)[tg])
+    assert 1e-9 < E < 1e-3
