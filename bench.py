@@ -217,13 +217,28 @@ def run_kitc(args, cfg, rank, world, local_rank):
     from paper_1902_02250_b200 import dist as D
     from paper_1902_02250_b200 import kitc
 
+    kern, n, theta, N0, eps, N = cfg["kernel"], cfg["n"], cfg["theta"], cfg["N0"], cfg["eps"], cfg["N"]
+    X, W = KI.config_particles(args.config)
+    # oracle baseline first: it forks worker processes, which must happen before CUDA is initialised
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        O.build()
+        procs = host_cores()
+        v1, det1, F1 = oracle_sample(cfg, X, W, 1500)
+        v, det, _ = oracle_sample(cfg, X, W, 200 * procs, seed=2, fhat=F1, procs=procs)
+        del F1
+        cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": "oracle",
+               "sample": f"full oracle tree (1 process); Algorithm 1 on clusters holding >=10% of sum N_C "
+                         f"(x sum N_C ratio) and Algorithm 2 on {200 * procs} random targets (x N/{200 * procs}), "
+                         f"split over {procs} processes of the single-threaded oracle (slowest timed)", **det,
+               "single_core": {"value": v1, "cores": 1, "eval_targets": 1500, **det1}}
+
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream()
-    kern, n, theta, N0, eps, N = cfg["kernel"], cfg["n"], cfg["theta"], cfg["N0"], cfg["eps"], cfg["N"]
     m, p = kitc.kitc_kernel_dims(kern)
     P3 = (n + 1) ** 3
-    X, W = KI.config_particles(args.config)
     Xd = torch.from_numpy(X).to(dev)
     Wd = torch.from_numpy(W).to(dev)
     T = kitc.Tree(Xd, N0)
@@ -386,18 +401,6 @@ def run_kitc(args, cfg, rank, world, local_rank):
             "algorithmic_flops_per_launch": flops_eval, "pairs_per_launch": pairs,
             "flops_per_pair": FLOPS_PER_PAIR[kern], "launch_ms": eval_launch_ms,
             "step_share": eval_launch_ms / ms_step}
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        import oracle as O
-        O.build()
-        procs = host_cores()
-        v1, det1, F1 = oracle_sample(cfg, X, W, 1500)
-        v, det, _ = oracle_sample(cfg, X, W, 200 * procs, seed=2, fhat=F1, procs=procs)
-        cpu = {"value": v, "unit": UNIT, "cores": procs, "kind": "oracle",
-               "sample": f"full oracle tree (1 process); Algorithm 1 on clusters holding >=10% of sum N_C "
-                         f"(x sum N_C ratio) and Algorithm 2 on {200 * procs} random targets (x N/{200 * procs}), "
-                         f"split over {procs} processes of the single-threaded oracle (slowest timed)", **det,
-               "single_core": {"value": v1, "cores": 1, "eval_targets": 1500, **det1}}
     line = {"metric": metric_for(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
