@@ -2,7 +2,7 @@
 # (C3 and C4), and the reference (oracle) arm.  Outputs under gpurun_out/.  usage: bash tools/gpu_round_bench.sh TAG
 TAG=${1:-v}
 mkdir -p gpurun_out
-for c in C3 C4 C5 C2 X2; do
+for c in C3 C4 C5 C2 X2 X1 X1L; do
   timeout 900 python bench.py --config $c > gpurun_out/bench_${c}_$TAG.json 2> gpurun_out/bench_${c}_$TAG.err; echo "bench $c rc=$?"
   tail -1 gpurun_out/bench_${c}_$TAG.json | cut -c1-200
 done
