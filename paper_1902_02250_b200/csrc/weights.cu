@@ -25,6 +25,9 @@ namespace kitc {
 
 namespace {
 
+#ifndef KITC_W_MINB
+#define KITC_W_MINB 6  // resident CTAs per SM (n <= 10); measured: 6 > 1 (128 regs) > 8 > 10
+#endif
 constexpr int kChunk = 4096;  // particles per work item
 constexpr int kTile = 64;     // particles staged per shared-memory tile
 
@@ -116,7 +119,7 @@ __device__ __forceinline__ void bary(double v, const double* s, double* L) {
 }
 
 template <int P, int M>
-__global__ void __launch_bounds__((P * P + 31) / 32 * 32) k_weights(
+__global__ void __launch_bounds__((P * P + 31) / 32 * 32, P <= 11 ? KITC_W_MINB : 1) k_weights(
     const WItem* __restrict__ items, const double* __restrict__ x, const double* __restrict__ y,
     const double* __restrict__ z, const double* __restrict__ ws, int N, const double* __restrict__ grid,
     const Peers fhat, double* __restrict__ part) {
