@@ -293,3 +293,22 @@ def test_C5_full_size_properties(K):
     assert O.rel_error(dref, dgot[:8]) <= DIRECT_GATE
     E = O.rel_error(dgot, host(out)[tg])
     assert 1e-9 < E < 1e-3
+
+
+def test_treecode_degenerate_inputs(K):
+    # coincident / duplicated / lattice points: degenerate leaves (count > N0), zero-size clusters
+    # accepted through their (n,n,n) proxy (reading A14), coincident non-self pairs at s = eps^2
+    rng = np.random.default_rng(4)
+    cases = [np.zeros((10, 3)),
+             np.array([[0, 0, 0]] * 30 + [[1, 1, 1]] * 30 + [[0.5, 0.2, 0.9]] * 5, float),
+             np.array([[i, j, k] for k in range(4) for j in range(4) for i in range(4)], float),
+             np.repeat(rng.uniform(-1, 1, (40, 3)), 7, axis=0)]
+    for X in cases:
+        W = rng.uniform(-1, 1, (X.shape[0], 3))
+        for self_omit in (True, False):
+            T = O.Tree(X, 3)
+            ref, rst = T.treecode(0, 0.05, 4, 0.7, W, self_omit=self_omit, stats=True)
+            got, gst, _ = run_gpu(K, X, W, 0, 4, 0.7, 3, 0.05, self_omit=self_omit)
+            assert np.array_equal(rst.astype(np.int64), gst)
+            if np.any(ref != 0):
+                assert O.rel_error(ref, got) <= TREE_GATE
