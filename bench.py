@@ -244,6 +244,14 @@ def run_kitc(args, cfg, rank, world, local_rank):
     T = kitc.Tree(Xd, N0)
     C = T.nclusters
     rg = T.export_ranges()
+    if world > 1:  # every rank must have built the identical tree (deterministic build): compare a checksum
+        h = torch.tensor([float(np.sum((rg["begin"] * 1000003 + rg["end"]) % 998244353)), float(C)],
+                         dtype=torch.float64, device=dev)
+        lo, hi = h.clone(), h.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        if not torch.equal(lo, hi):
+            raise RuntimeError("ranks built different trees")
     cshards = D.cluster_shards(rg["begin"], rg["end"], world, skip_root=True)
     S = D.padded_shard_size(cshards)
     cb, ce = cshards[rank]
