@@ -255,6 +255,22 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
                         }
                     }
                     K::row_end(dx, dy, r, acc);
+                } else if (KITC_DZ_SMEM && (P2 - RF * kRows == 2 || P2 - RF * kRows == 4)) {
+                    // partial block of 2 or 4 rows (even P): kRows / nrem lanes per row, each
+                    // summing a contiguous k3 range in row form (partial row sums are linear)
+                    const int nrem = P2 - RF * kRows, L = kRows / max(nrem, 1), KL = (P + L - 1) / L;
+                    const int jj = grp / L, q = grp - jj * L, row = RF * kRows + jj;
+                    const int k1 = row / P, k2 = row - k1 * P;
+                    const double dx = x - __ldg(g + k1), dy = y - __ldg(g + P + k2);
+                    const double pxye = fma(dy, dy, dx * dx) + kp.e2;
+                    typename K::Row r;
+                    for (int k3 = q * KL; k3 < min(P, (q + 1) * KL); ++k3) {
+                        double f[M];
+#pragma unroll
+                        for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + jj];
+                        K::pair_row(dx, dy, dz[k3], fma(dz[k3], dz[k3], pxye), f, acc, r, kp);
+                    }
+                    K::row_end(dx, dy, r, acc);
                 } else {  // partial last block: pair by pair
                     const int pairs = (P2 - RF * kRows) * P;
                     for (int q = grp; q < pairs; q += kRows) {
