@@ -13,7 +13,9 @@
  * "Readings of the paper").
  *
  * Pinned by tests/test_oracle_*.py (-m "not gpu") against closed forms,
- * invariants and brute force -- see DESIGN.md "Oracle pins".
+ * invariants and brute force -- see DESIGN.md "Oracle pins" (including the
+ * separate-target functions, test_oracle_targets.py, and the size-check
+ * variant, test_oracle_sizecheck.py).
  */
 #include <float.h>
 #include <math.h>
