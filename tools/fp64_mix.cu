@@ -17,6 +17,7 @@ __global__ void k(double* out, int iters) {
       if (MODE == 3) a[c] = seed(a[c]) + 1.0;  // 1 MUFU + 1 DADD
       if (MODE == 4) { double y = seed(a[c]); a[c] = fma(fma(fma(fma(y, m, b), m, b), m, b), m, 1.0); } // 1 MUFU + 4 DFMA
       if (MODE == 5) { double y = a[c]; a[c] = fma(fma(fma(fma(y, m, b), m, b), m, b), m, 1.0); }  // 4 DFMA (same dep shape)
+      if (MODE == 6) { double y = (double)rsqrtf((float)a[c]); a[c] = fma(fma(fma(fma(y, m, b), m, b), m, b), m, 1.0); } // F2F+MUFU.RSQ+F2F + 4 DFMA
     }
   }
   double s = 0;
@@ -38,5 +39,6 @@ int main() {
   double* o; cudaMalloc(&o, 8);
   run<0>("DFMA", 1, o, sms, clk); run<1>("DMUL", 1, o, sms, clk); run<2>("DADD", 1, o, sms, clk);
   run<3>("MUFU.RSQ64H + DADD", 1, o, sms, clk); run<4>("MUFU.RSQ64H + 4 DFMA", 4, o, sms, clk); run<5>("4 DFMA", 4, o, sms, clk);
+  run<6>("F2F+MUFU.RSQ(f32)+F2F + 4 DFMA", 4, o, sms, clk);
   return 0;
 }
