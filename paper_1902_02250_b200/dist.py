@@ -90,7 +90,7 @@ class PeerFhat:
     def modified_weights(self, T, kernel, n, W, cluster_range, stream=None):
         from . import kitc
         cb, ce = cluster_range
-        self.hdl.barrier(channel=0)
+        self.hdl.barrier(channel=0)   # no rank still reads the previous step's fhat
         kitc.kitc_modified_weights_peers(T.handle, kernel, n, kitc._ptr(W), cb, ce, self.ptrs, kitc._stream(stream))
-        self.hdl.barrier(channel=0)
+        self.hdl.barrier(channel=1)   # every replica complete
         return self.fhat
