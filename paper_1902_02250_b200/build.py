@@ -32,11 +32,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
         nvcc = "/usr/local/cuda/bin/nvcc"
     cus = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
+    objdir = os.path.join(ROOT, "build", "kitc_obj")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    jobs = []
+    for cu in cus:  # one nvcc per translation unit, in parallel (eval.cu dominates)
+        obj = os.path.join(objdir, os.path.basename(cu) + ".o")
+        cmd = [nvcc, *cflags, "-c", "-o", obj, cu]
+        if verbose:
+            print(" ".join(cmd))
+        jobs.append((subprocess.Popen(cmd), obj))
+    objs = []
+    for proc, obj in jobs:
+        if proc.wait() != 0:
+            raise subprocess.CalledProcessError(proc.returncode, "nvcc -c " + obj)
+        objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, "-o", tmp, *cus]
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+        print(" ".join(link))
+    subprocess.check_call(link)
     os.replace(tmp, LIB)
     return LIB
 
