@@ -29,7 +29,10 @@ namespace {
 #define KITC_W_MINB 6  // resident CTAs per SM (n <= 10); measured: 6 > 1 (128 regs) > 8 > 10
 #endif
 constexpr int kChunk = 4096;  // particles per work item
-constexpr int kTile = 64;     // particles staged per shared-memory tile
+#ifndef KITC_W_TILE
+#define KITC_W_TILE 32  // measured: 32 > 64 > 16
+#endif
+constexpr int kTile = KITC_W_TILE;  // particles staged per shared-memory tile
 
 struct WItem {
     int32_t c;     // cluster id
