@@ -36,7 +36,10 @@ namespace {
 #define KITC_EVAL_MINB 5  // resident CTAs per SM (register budget), Stokeslet (measured: 5 > 4 > 6 with dz in smem)
 #endif
 #ifndef KITC_EVAL_MINB_P8
-#define KITC_EVAL_MINB_P8 4  // Stokeslet at n = 7 (measured: 4 beats 5 on X1 / X1L)
+#define KITC_EVAL_MINB_P8 4  // Stokeslet at n = 7, 9, 10 (measured: 4 beats 5 on X1 / X1L and the C2 sweep)
+#endif
+#ifndef KITC_EVAL_MINB_OTHER
+#define KITC_EVAL_MINB_OTHER 5  // Stokeslet at n <= 6 (measured: 5 beats 4 on the C2 sweep)
 #endif
 #ifndef KITC_EVAL_MINB1
 #define KITC_EVAL_MINB1 4  // rotlet / combined (measured: 4 beats 5 and 6 on C4)
@@ -573,7 +576,7 @@ __device__ __forceinline__ void near_leaf(double x, double y, double z, int t, i
 // group; the kGroup lanes of a target share every MAC decision.
 // STATS: also write the per-target interaction counts (a.stats != nullptr).
 template <int PT, int KER, bool STATS>
-__global__ void __launch_bounds__(kWarps * 32, KER == 0 ? (PT == 8 ? KITC_EVAL_MINB_P8 : KITC_EVAL_MINB) : KITC_EVAL_MINB1) k_eval(const EvalArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, KER == 0 ? (PT == 9 ? KITC_EVAL_MINB : (PT == 8 || PT >= 10) ? KITC_EVAL_MINB_P8 : KITC_EVAL_MINB_OTHER) : KITC_EVAL_MINB1) k_eval(const EvalArgs a) {
     using K = EvalKern<KER>;
     constexpr int M = K::M, NP = K::P, NA = K::NA;
     extern __shared__ __align__(128) unsigned char smem_raw[];

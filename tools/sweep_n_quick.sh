@@ -1,4 +1,4 @@
-for v in default prev; do
+for v in default; do
   if [ $v = default ]; then unset KITC_LIB; else export KITC_LIB=$PWD/tools/variants/libkitc_$v.so; fi
   python - <<'PY'
 import sys, os, torch
@@ -9,7 +9,7 @@ X, W = KI.config_particles("C2")
 Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
 G = kitc.Tree(Xd, 500)
 res = []
-for n in (1, 5, 8, 9):
+for n in (1, 2, 3, 4, 5, 6, 9, 10):
     fh = G.modified_weights(0, n, Wd)
     out = G.eval(0, n, 0.7, 0.01, fh)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
