@@ -1,10 +1,11 @@
 // direct.cu -- O(N^2) direct sum u(x_i) = sum_j k(x_i, y_j) f_j (Eq. N-body,
 // P:42-67) and the relative error E (Eq. error), sm_100a fp64.
 //
-// One thread per target; sources are staged through shared memory in tiles of
-// kTile (broadcast reads); each tile's contribution is summed into a tile
-// partial that is then added to the running total (two-level summation keeps
-// the rounding of N = 1e7 sums ~10x below the 1e-12 parity gate).
+// Two targets per thread (two independent pair chains); sources are staged
+// through shared memory in tiles of kTile (broadcast reads); each tile's
+// contribution is summed into a tile partial that is then added to the running
+// total (two-level summation keeps the rounding of N = 1e7 sums ~10x below the
+// 1e-12 parity gate).  The self-pair test runs only in tiles that can hold it.
 #include <algorithm>
 #include <cmath>
 
@@ -17,8 +18,43 @@ namespace {
 
 constexpr int kTile = 256;
 
+#ifndef KITC_DIRECT_TPT
+#define KITC_DIRECT_TPT 1  // measured at N = 1e6: 1 (55.2% of FP64 peak) ~ 3 > 2 > 4
+#endif
+constexpr int kTPT = KITC_DIRECT_TPT;  // targets per thread (independent pair chains per source)
+
+// The source tile's contribution to one target; SELF: the tile may hold the
+// target's own source `si` -- that pair is evaluated with f = 0, s = 1 (an exact
+// zero), otherwise no per-pair test at all.
+template <int KER, bool SELF>
+__device__ __forceinline__ void tile_pairs(const double* x, const double* y, const double* z, const long long* si,
+                                           int tile, int cnt, const double* sx, const double* sy, const double* sz,
+                                           const double (*sw)[kTile], double (*part)[Kern<KER>::P],
+                                           const KParams& kp) {
+    using K = Kern<KER>;
+    constexpr int M = K::M;
+    for (int jj = 0; jj < cnt; ++jj) {
+        double f[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) f[m] = sw[m][jj];
+        const double xj = sx[jj], yj = sy[jj], zj = sz[jj];
+#pragma unroll
+        for (int q = 0; q < kTPT; ++q) {
+            const double dx = x[q] - xj, dy = y[q] - yj, dz = z[q] - zj;
+            const bool me = SELF && (tile + jj == si[q]);
+            double g[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) g[m] = me ? 0.0 : f[m];
+            const double s = me ? 1.0 : fma(dx, dx, fma(dy, dy, fma(dz, dz, kp.e2)));
+            K::pair(dx, dy, dz, s, g, part[q], kp);
+        }
+    }
+}
+
 // tidx (optional): target q is source tidx[q] (sampled targets; its self pair is
 // the one skipped under SELF_OMIT); otherwise target q is xt[q] (self = q).
+// Each thread owns kTPT targets (i, i + kTile); summation order per target is
+// sources ascending within a tile, tiles ascending (two-level).
 template <int KER>
 __global__ void __launch_bounds__(kTile) k_direct(const double* __restrict__ xt, int Nt,
                                                   const long long* __restrict__ tidx,
@@ -28,19 +64,29 @@ __global__ void __launch_bounds__(kTile) k_direct(const double* __restrict__ xt,
     using K = Kern<KER>;
     constexpr int M = K::M, NP = K::P;
     __shared__ double sx[kTile], sy[kTile], sz[kTile], sw[M][kTile];
-    const int i = blockIdx.x * kTile + threadIdx.x;
-    const bool valid = i < Nt;
-    double x = 0, y = 0, z = 0;
-    long long si = i;
-    if (valid) {
-        const double* p = tidx ? xs + 3 * (si = tidx[i]) : xt + 3 * (size_t)i;
-        x = p[0];
-        y = p[1];
-        z = p[2];
-    }
-    double tot[NP];
+    double x[kTPT], y[kTPT], z[kTPT];
+    long long si[kTPT];
+    int ii[kTPT];
 #pragma unroll
-    for (int c = 0; c < NP; ++c) tot[c] = 0.0;
+    for (int q = 0; q < kTPT; ++q) {
+        ii[q] = blockIdx.x * (kTPT * kTile) + q * kTile + threadIdx.x;
+        si[q] = self_omit ? ii[q] : -1;
+        x[q] = y[q] = z[q] = 0.0;
+        if (ii[q] < Nt) {
+            const double* p = tidx ? xs + 3 * tidx[ii[q]] : xt + 3 * (size_t)ii[q];
+            if (tidx && self_omit) si[q] = tidx[ii[q]];
+            x[q] = p[0];
+            y[q] = p[1];
+            z[q] = p[2];
+        } else {
+            si[q] = -1;
+        }
+    }
+    double tot[kTPT][NP];
+#pragma unroll
+    for (int q = 0; q < kTPT; ++q)
+#pragma unroll
+        for (int c = 0; c < NP; ++c) tot[q][c] = 0.0;
     for (int tile = 0; tile < Ns; tile += kTile) {
         const int j = tile + threadIdx.x;
         if (j < Ns) {
@@ -52,24 +98,29 @@ __global__ void __launch_bounds__(kTile) k_direct(const double* __restrict__ xt,
         }
         __syncthreads();
         const int cnt = min(kTile, Ns - tile);
-        double part[NP];
+        double part[kTPT][NP];
 #pragma unroll
-        for (int c = 0; c < NP; ++c) part[c] = 0.0;
-        for (int jj = 0; jj < cnt; ++jj) {
-            const double dx = x - sx[jj], dy = y - sy[jj], dz = z - sz[jj];
-            double f[M];
+        for (int q = 0; q < kTPT; ++q)
 #pragma unroll
-            for (int m = 0; m < M; ++m) f[m] = sw[m][jj];
-            const double s = fma(dx, dx, fma(dy, dy, fma(dz, dz, kp.e2)));
-            if (!self_omit || tile + jj != si) K::pair(dx, dy, dz, s, f, part, kp);
-        }
+            for (int c = 0; c < NP; ++c) part[q][c] = 0.0;
+        bool mine = false;
 #pragma unroll
-        for (int c = 0; c < NP; ++c) tot[c] += part[c];
+        for (int q = 0; q < kTPT; ++q) mine |= si[q] >= tile && si[q] < tile + cnt;
+        if (__any_sync(0xffffffffu, mine))  // warp-uniform: some lane's own source is in this tile
+            tile_pairs<KER, true>(x, y, z, si, tile, cnt, sx, sy, sz, sw, part, kp);
+        else
+            tile_pairs<KER, false>(x, y, z, si, tile, cnt, sx, sy, sz, sw, part, kp);
+#pragma unroll
+        for (int q = 0; q < kTPT; ++q)
+#pragma unroll
+            for (int c = 0; c < NP; ++c) tot[q][c] += part[q][c];
         __syncthreads();
     }
-    if (valid)
 #pragma unroll
-        for (int c = 0; c < NP; ++c) out[(size_t)i * NP + c] = tot[c] * K::scale(c);
+    for (int q = 0; q < kTPT; ++q)
+        if (ii[q] < Nt)
+#pragma unroll
+            for (int c = 0; c < NP; ++c) out[(size_t)ii[q] * NP + c] = tot[q][c] * K::scale(c);
 }
 
 constexpr int kErrBlocks = 592;  // 4 x 148 SMs; fixed -> deterministic
@@ -115,7 +166,7 @@ kitc_status direct(int kernel, double eps, int self, const double* xt, int64_t N
     if (Nt == 0) return KITC_OK;
     if (!xt || !out || (Ns > 0 && (!xs || !ws))) return set_error(KITC_EINVAL, "kitc_direct: NULL buffer");
     const KParams kp = make_kparams(eps);
-    const int grid = (int)((Nt + kTile - 1) / kTile);
+    const int grid = (int)((Nt + kTPT * kTile - 1) / (kTPT * kTile));
     const int so = self == KITC_SELF_OMIT;
     switch (kernel) {
         case KITC_STOKESLET: k_direct<0><<<grid, kTile, 0, s>>>(xt, (int)Nt, reinterpret_cast<const long long*>(tidx), xs, ws, (int)Ns, out, kp, so); note_launch(); break;

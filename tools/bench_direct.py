@@ -20,5 +20,5 @@ e1.record()
 e1.synchronize()
 ms = e0.elapsed_time(e1) / 3
 pairs = N * (N - 1)
-print(f"direct N={N}: {ms:.2f} ms, {pairs / ms / 1e9:.1f} Gpairs/s, {32 * pairs / ms / 1e9:.2f} TFLOP/s algorithmic "
+print(f"direct N={N}: {ms:.2f} ms, {pairs / ms / 1e6:.1f} Gpairs/s, {32 * pairs / ms / 1e9:.2f} TFLOP/s algorithmic "
       f"({32 * pairs / ms / 1e9 / 37.2249:.3f} of 37.22)")
