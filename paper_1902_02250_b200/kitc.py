@@ -111,6 +111,15 @@ def _dev_f64(t, shape1):
     return t
 
 
+def _buf_f64(t, numel, what):
+    """A caller-provided device buffer the kernels index: contiguous fp64 CUDA, exact size."""
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError(f"{what}: expected a contiguous float64 CUDA tensor")
+    if t.numel() != numel:
+        raise ValueError(f"{what}: expected {numel} elements, got {t.numel()}")
+    return t
+
+
 # ---- raw C entry points (same names as include/kitc.h) -----------------------
 
 def kitc_kernel_dims(kernel):
@@ -231,6 +240,7 @@ class Tree:
         W = _dev_f64(W, m)
         if fhat is None:
             fhat = torch.empty(self.fhat_shape(kernel, n), dtype=torch.float64, device=W.device)
+        _buf_f64(fhat, self.nclusters * kitc_fhat_cluster_len(kernel, n), "fhat")
         cb, ce = cluster_range if cluster_range is not None else (0, self.nclusters)
         kitc_modified_weights(self._h, kernel, n, _ptr(W), cb, ce, _ptr(fhat), _stream(stream))
         return fhat
@@ -239,9 +249,11 @@ class Tree:
              stats=False, stream=None, size_check=False, part=None):
         """part=(p, k): interleaved part p of k (kitc_eval_part) instead of a batch range."""
         _, p = kitc_kernel_dims(kernel)
+        _buf_f64(fhat, self.nclusters * kitc_fhat_cluster_len(kernel, n), "fhat")
         dev = fhat.device
         if out is None:
             out = torch.zeros((self.N, p), dtype=torch.float64, device=dev)
+        _buf_f64(out, self.N * p, "out")
         st = torch.zeros((self.N, 5), dtype=torch.int64, device=dev) if stats else None
         if part is not None:
             _call("kitc_eval_part", self._h, int(kernel), int(n), float(theta), self.N0, float(eps),
@@ -257,8 +269,10 @@ class Tree:
         """Treecode at a separate target set Xt[Nt, 3] (device fp64); no self term."""
         _, p = kitc_kernel_dims(kernel)
         Xt = _dev_f64(Xt, 3)
+        _buf_f64(fhat, self.nclusters * kitc_fhat_cluster_len(kernel, n), "fhat")
         if out is None:
             out = torch.zeros((Xt.shape[0], p), dtype=torch.float64, device=Xt.device)
+        _buf_f64(out, Xt.shape[0] * p, "out")
         st = torch.zeros((Xt.shape[0], 5), dtype=torch.int64, device=Xt.device) if stats else None
         kitc_eval_targets_ex(self._h, kernel, n, theta, self.N0, eps, EVAL_SIZE_CHECK if size_check else 0,
                              _ptr(fhat), _ptr(Xt), Xt.shape[0], _ptr(out), _ptr(st), _stream(stream))
@@ -309,6 +323,7 @@ def direct(X, W, kernel, eps, self_omit=True, targets=None, out=None, stream=Non
     T = X if targets is None else _dev_f64(targets, 3)
     if out is None:
         out = torch.empty((T.shape[0], p), dtype=torch.float64, device=X.device)
+    _buf_f64(out, T.shape[0] * p, "out")
     kitc_direct(kernel, eps, SELF_OMIT if self_omit else SELF_INCLUDE, _ptr(T), T.shape[0], _ptr(X),
                 _ptr(W), X.shape[0], _ptr(out), _stream(stream))
     return out
@@ -321,6 +336,7 @@ def direct_sample(X, W, kernel, eps, idx, self_omit=True, out=None, stream=None)
     idx = idx.to(device=X.device, dtype=torch.int64).contiguous()
     if out is None:
         out = torch.empty((idx.numel(), p), dtype=torch.float64, device=X.device)
+    _buf_f64(out, idx.numel() * p, "out")
     _call("kitc_direct_sample", int(kernel), float(eps), SELF_OMIT if self_omit else SELF_INCLUDE, _ptr(idx),
           idx.numel(), _ptr(X), _ptr(W), X.shape[0], _ptr(out), _stream(stream))
     return out

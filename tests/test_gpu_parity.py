@@ -206,8 +206,9 @@ def test_state_errors(K):
         G.eval(0, 4, 0.7, 0.01, fh)                          # weights not computed
     assert e.value.status == K.KITC_ESTATE
     G.modified_weights(0, 4, dev(W), fhat=fh)
-    with pytest.raises(K.KitcError):
-        G.eval(0, 5, 0.7, 0.01, fh)                          # n mismatch
+    with pytest.raises(K.KitcError) as e:                    # n mismatch (C-ABI state check)
+        K.kitc_eval(G.handle, 0, 5, 0.7, 50, 0.01, 0, K._ptr(fh), 0, 1, K._ptr(fh), None, K._stream())
+    assert e.value.status == K.KITC_ESTATE
     with pytest.raises(K.KitcError):
         K.kitc_eval(G.handle, 0, 4, 0.7, 51, 0.01, 0, K._ptr(fh), 0, 1, K._ptr(fh), None, K._stream())
     with pytest.raises(K.KitcError):

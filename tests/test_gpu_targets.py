@@ -76,8 +76,10 @@ def test_eval_targets_empty_and_errors(K):
     fh = G.modified_weights(0, 4, dev(W))
     out = G.eval_targets(0, 4, 0.7, 0.01, fh, torch.zeros((0, 3), dtype=torch.float64, device="cuda"))
     assert out.shape == (0, 3)
-    with pytest.raises(K.KitcError):
-        G.eval_targets(0, 5, 0.7, 0.01, fh, dev(targets(10, 0)))     # n mismatch
+    xt = dev(targets(10, 0))
+    ot = torch.zeros((10, 3), dtype=torch.float64, device="cuda")
+    with pytest.raises(K.KitcError):                                 # n mismatch (C-ABI state check)
+        K.kitc_eval_targets(G.handle, 0, 5, 0.7, 50, 0.01, K._ptr(fh), K._ptr(xt), 10, K._ptr(ot), None, K._stream())
     with pytest.raises(K.KitcError):
         G.eval_targets(0, 4, 1.0, 0.01, fh, dev(targets(10, 0)))     # theta >= 1
 
@@ -169,3 +171,20 @@ def test_peer_fhat_world1(K):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_binding_rejects_wrong_buffers(K):
+    # the binding checks the buffers the kernels index (size, dtype, device) before any launch
+    X, W = KI.particles(500, seed=1)
+    G = K.Tree(dev(X), 50)
+    fh = G.modified_weights(0, 4, dev(W))
+    with pytest.raises(ValueError):
+        G.eval(0, 4, 0.7, 0.01, fh[:-1])                       # short fhat
+    with pytest.raises(ValueError):
+        G.eval(0, 5, 0.7, 0.01, fh)                            # fhat sized for n = 4
+    with pytest.raises(ValueError):
+        G.eval(0, 4, 0.7, 0.01, fh, out=torch.zeros((499, 3), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        G.eval_targets(0, 4, 0.7, 0.01, fh.float(), dev(targets(5, 0)))
+    with pytest.raises(ValueError):
+        K.direct(dev(X), dev(W), 0, 0.01, out=torch.zeros((500, 2), dtype=torch.float64, device="cuda"))
