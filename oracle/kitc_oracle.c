@@ -705,8 +705,8 @@ int orc_direct(int kernel, double eps, int poly_deg, int self_omit, int64_t N, c
     return 0;
 }
 
-/* u(x_q) = sum_j k(x_q, y_j) f_j at separate targets xt (nt x 3), all j
- * ascending (no self term). */
+/* u(x_q) = sum_j k(x_q, y_j) f_j (Eq. N-body) at separate targets xt
+ * (nt x 3), all j ascending (no self term: no target is a source). */
 int orc_direct_targets(int kernel, double eps, int poly_deg, int64_t N, const double* xyz,
                        const double* w, const double* xt, int64_t nt, double* out)
 {
