@@ -272,12 +272,18 @@ def run_kitc(args, cfg, rank, world, local_rank):
     use_p2p = world > 1 and args.exchange == "p2p"
     if use_p2p:
         # fused weights + exchange over peer memory; cross-checked bitwise against the NCCL path
+        why = ""
         try:
             pf = D.PeerFhat(C, L, dev)
             fhat_p2p = pf.modified_weights(T, kern, n, Wd, (cb, ce))
+            torch.cuda.synchronize()
         except Exception as ex:  # symmetric memory unavailable on this node: say so, use NCCL
+            why = f"{type(ex).__name__}: {ex}"
+        okf = torch.tensor([0 if why else 1], device=dev)
+        dist.all_reduce(okf, op=dist.ReduceOp.MIN)   # one decision for all ranks
+        if int(okf[0]) != 1:
             use_p2p = False
-            exchange = f"NCCL all_gather_into_tensor (peer-memory path unavailable: {type(ex).__name__}: {ex})"[:300]
+            exchange = f"NCCL all_gather_into_tensor (peer-memory path unavailable: {why or 'on another rank'})"[:300]
     if use_p2p:
         weights_nccl()
         torch.cuda.synchronize()
