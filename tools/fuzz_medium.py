@@ -16,7 +16,7 @@ from paper_1902_02250_b200 import kitc  # noqa: E402
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 bad = 0
 for case in range(cases):
-    rng = np.random.default_rng(5000 + case)
+    rng = np.random.default_rng(5000 + case + int(os.environ.get("FUZZ_OFFSET", "0")))
     kern = int(rng.integers(0, 3))
     geom = ["uniform", "sphere", "slab", "organisms"][int(rng.integers(0, 4))]
     if geom == "organisms":
