@@ -128,3 +128,30 @@ def test_organisms_generator_matches_paper_example1():
     assert np.allclose(W[0::2], d / 0.02, atol=1e-12) and np.array_equal(W[1::2], -W[0::2])
     assert X[0::2].min() >= 0 and X[0::2].max() <= 10
     assert KI.CONFIGS["X1"]["N"] == 640_000 and KI.CONFIGS["X1L"]["N"] == 5_120_000   # Table 1 rows
+
+
+def test_plain_c_client(lib, tmp_path):
+    # the boundary is a C ABI: a C99 program includes kitc.h, links libkitc.so and calls it
+    # (no torch, no Python), exercising the argument checks that need no GPU
+    from paper_1902_02250_b200 import build as B
+    src = tmp_path / "client.c"
+    src.write_text(r"""
+#include "kitc.h"
+#include <stdio.h>
+int main(void) {
+    int64_t len = 0;
+    int32_t m = 0, p = 0;
+    if (kitc_fhat_cluster_len(KITC_ROTLET, 8, &len) != KITC_OK || len != 11 * 9 * 3 * 8) return 1;
+    if (kitc_kernel_dims(KITC_STOKESLET_ROTLET, &m, &p) != KITC_OK || m != 6 || p != 6) return 2;
+    if (kitc_fhat_cluster_len(KITC_STOKESLET, 17, &len) != KITC_EINVAL) return 3;
+    if (kitc_last_error()[0] == 0) return 4;
+    puts("ok");
+    return 0;
+}
+""")
+    exe = tmp_path / "client"
+    libdir = os.path.dirname(B.LIB)
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
+                           "-L", libdir, "-lkitc", f"-Wl,-rpath,{libdir}", "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", (out.returncode, out.stdout, out.stderr)
