@@ -62,7 +62,18 @@ namespace {
 #ifndef KITC_EVAL_SB
 #define KITC_EVAL_SB 2
 #endif
+#ifndef KITC_FAR_TB
+// far field with all 4 targets accepting: one row for TWO targets per lane, Stokeslet at
+// P = 8, 10 (measured on the C3 input: n = 7 -8%, n = 9 -6%; slower at P = 9 (spills at
+// 5 CTAs/SM, 4 CTAs/SM loses more), P = 11, P <= 7 and for the rotlet)
+#define KITC_FAR_TB 1
+#endif
 constexpr int kWarps = KITC_EVAL_WARPS;  // warps (batches) per CTA
+template <int PT, int KER>
+__host__ __device__ constexpr int eval_min_blocks() {  // CTAs/SM per instantiation (measured, see the macros above)
+    return KER == 0 ? (PT == 9 ? KITC_EVAL_MINB : (PT == 8 || PT >= 10) ? KITC_EVAL_MINB_P8 : KITC_EVAL_MINB_OTHER)
+                    : KITC_EVAL_MINB1;
+}
 constexpr int kPartChunk = 64;          // batches per chunk of the interleaved multi-GPU split
 #ifdef KITC_EVAL_HIST
 __device__ unsigned long long g_hist[10];
@@ -188,11 +199,54 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
         for (int k3 = 0; k3 < PT; ++k3) dz[k3] = z - __ldg(g + 2 * PT + k3);
     }
 #endif
+#if KITC_FAR_TB
+    // register blocking over targets (all 4 accept): lane L evaluates row L & 15 of the
+    // stage for its own target (acc) and for the sibling target of lane L ^ 8 (oth); the
+    // f-hat row is read once for both, and oth is folded into the sibling's lanes below
+    constexpr bool kTB = KITC_FAR_TB && KITC_DZ_SMEM && K::kPairRows && kSB == 2 && KER == 0 &&
+                         (PT == 8 || PT == 10);
+    const bool tb = kTB && am == 0xffffffffu;
+    double oth[K::NA];
+    double ox = 0.0, oy = 0.0;
+    if constexpr (kTB) if (tb) {
+#pragma unroll
+        for (int c = 0; c < K::NA; ++c) oth[c] = 0.0;
+        ox = __shfl_xor_sync(0xffffffffu, x, kGroup);
+        oy = __shfl_xor_sync(0xffffffffu, y, kGroup);
+    }
+#endif
     for (int st = 0; st < NS; ++st) {
         const int k = base + st;
         const double* B = ws.buf + (k & 1) * kSB * blk;
         mbar_wait(ws.bar + (k & 1), (unsigned)(k >> 1) & 1u);
         const int b0 = st * kSB;  // first block of the stage
+#if KITC_FAR_TB
+        if (kTB && tb && b0 + 1 < RF) {
+            const int q = lane & 15, h = q >> 3, j = q & 7;
+            const int row = (b0 + h) * kRows + j;
+            const int k1 = row / P, k2 = row - k1 * P;
+            const double gx = __ldg(g + k1), gy = __ldg(g + P + k2);
+            const double dxa = x - gx, dya = y - gy, dxb = ox - gx, dyb = oy - gy;
+            const double pa = fma(dya, dya, dxa * dxa) + kp.e2;
+            const double pb = fma(dyb, dyb, dxb * dxb) + kp.e2;
+            const double* Bj = B + h * blk + j;
+            const double* dzb = ws.dzs + ((lane / kGroup) ^ 1) * P;  // the sibling target's dz
+            typename K::Row rA, rB;
+            if constexpr (PT > 0) {
+#pragma unroll
+                for (int k3 = 0; k3 < PT; ++k3) {
+                    double f[M];
+#pragma unroll
+                    for (int m = 0; m < M; ++m) f[m] = Bj[(k3 * M + m) * kRows];
+                    const double za = dz[k3], zb = dzb[k3];
+                    K::pair_row(dxa, dya, za, fma(za, za, pa), f, acc, rA, kp);
+                    K::pair_row(dxb, dyb, zb, fma(zb, zb, pb), f, oth, rB, kp);
+                }
+            }
+            K::row_end(dxa, dya, rA, acc);
+            K::row_end(dxb, dyb, rB, oth);
+        } else
+#endif
         if (K::kPairRows && kSB == 2 && b0 + 1 < RF) {
             // two full blocks: rows ra, ra + 1 of block h = grp / 4
             const int h = grp >> 2, j = 2 * (grp & 3);
@@ -299,6 +353,12 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
         }
     }
     if (leader) *ws.nround = base + NS;
+#if KITC_FAR_TB
+    if constexpr (kTB) if (tb) {
+#pragma unroll
+        for (int c = 0; c < K::NA; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, oth[c], kGroup);
+    }
+#endif
     __syncwarp(am);
 }
 
@@ -576,7 +636,7 @@ __device__ __forceinline__ void near_leaf(double x, double y, double z, int t, i
 // group; the kGroup lanes of a target share every MAC decision.
 // STATS: also write the per-target interaction counts (a.stats != nullptr).
 template <int PT, int KER, bool STATS>
-__global__ void __launch_bounds__(kWarps * 32, KER == 0 ? (PT == 9 ? KITC_EVAL_MINB : (PT == 8 || PT >= 10) ? KITC_EVAL_MINB_P8 : KITC_EVAL_MINB_OTHER) : KITC_EVAL_MINB1) k_eval(const EvalArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eval(const EvalArgs a) {
     using K = EvalKern<KER>;
     constexpr int M = K::M, NP = K::P, NA = K::NA;
     extern __shared__ __align__(128) unsigned char smem_raw[];

@@ -139,6 +139,8 @@ def run_gpu(K, X, W, kern, n, theta, N0, eps, self_omit=True):
     (4000, 100, 5, 0.7, 0, 0.0, "uniform"),       # eps = 0: the singular (classical) Stokeslet
     (1500, 40, 16, 0.7, 1, 0.01, "uniform"),      # maximum degree n = 16 (runtime-P kernel), rotlet
     (2500, 80, 6, 0.95, 2, 0.02, "slab"),         # theta close to 1, combined kernel, 4-way splits
+    (20000, 300, 7, 0.7, 0, 0.01, "uniform"),     # P = 8: far field blocked over target pairs
+    (12001, 250, 9, 0.6, 0, 0.01, "uniform"),     # P = 10: the same, odd N
 ])
 def test_treecode_parity(K, N, N0, n, theta, kern, eps, geom):
     m = O.DIMS[kern][0]

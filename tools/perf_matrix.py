@@ -1,5 +1,5 @@
 """Eval throughput over (n, theta) on the C3 input (N = 1e6 uniform, N0 = 2000, Stokeslet and rotlet):
-eval ms, pairs/target, % of the derived FP64 peak.  python tools/perf_matrix.py"""
+eval ms, pairs/target, % of the derived FP64 peak.  [PM_N=4,6 PM_THETA=0.7] python tools/perf_matrix.py"""
 import json
 import os
 import sys
@@ -16,10 +16,12 @@ X, W = KI.config_particles("C3")
 Xd, Wd = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
 G = kitc.Tree(Xd, 2000)
 rows = []
+NS = [int(v) for v in os.environ.get("PM_N", "4,6,8,10").split(",")]
+THETAS = [float(v) for v in os.environ.get("PM_THETA", "0.5,0.7").split(",")]
 for kern in (0, 1):
-    for n in (4, 6, 8, 10):
+    for n in NS:
         fh = G.modified_weights(kern, n, Wd)
-        for theta in (0.5, 0.7):
+        for theta in THETAS:
             out, st = G.eval(kern, n, theta, 0.01, fh, stats=True)
             pairs = int(st[:, 1].sum() + st[:, 3].sum())
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
