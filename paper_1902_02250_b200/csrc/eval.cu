@@ -11,9 +11,10 @@
 //   far   accepting lanes sum the kernel against the (n+1)^3 proxies s_k with the
 //         modified weights fhat_k (Eq. pc_approximation_3D): fhat
 //         staged into shared memory by cp.async.bulk (TMA) two stages ahead,
-//         tensor-product reuse of dx, dy, dz, two rows per lane (far_field); a
-//         cluster accepted by only 1 or 2 targets is done by the whole warp
-//         (far_field_team)
+//         tensor-product reuse of dx, dy, dz, two rows per lane (far_field) or,
+//         for the Stokeslet at P = 8, 10 with all 4 targets accepting, one row
+//         for two targets per lane; a cluster accepted by only 1 or 2 targets is
+//         done by the whole warp (far_field_team)
 //   near  rejecting lanes at a leaf sum over its particles directly
 //         (Eq. pc_interaction_3D), j == i skipped by index (reading A8); idle
 //         target groups join 1 or 2 participating targets (near_leaf)
