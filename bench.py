@@ -55,7 +55,18 @@ def parse():
     ap.add_argument("--no-check", action="store_true", help="skip E vs the GPU direct sum")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 fhat exchange: fused peer-memory stores (default) or NCCL all-gather")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check: start the ranks, one all-reduce (gloo without a GPU), print the rank count")
     return ap.parse_args()
+
+
+def workload(config):
+    """The `config.workload` string -- identical in both arms."""
+    return f"{config} ({KI.CONFIGS[config]})"
+
+
+PRECISION = ("fp64 throughout; the treecode evaluation's s^-1/2 is one Newton step from the MUFU seed "
+             "(relative error < 2e-12, DESIGN.md reading A19); the direct sum keeps ~4 ulp")
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -152,15 +163,17 @@ def oracle_sample(cfg, X, W, S_targets, weight_frac=0.1, seed=1, fhat=None, proc
     m = O.DIMS[cfg["kernel"]][0]
     F = np.zeros((T.nclusters, m, (cfg["n"] + 1) ** 3)) if fhat is None else fhat.copy()
     tg = KI.sample_targets(N, S_targets, seed=seed)
+    w_scale = tot / acc if acc > 0 else 0.0
+    e_scale = N / len(tg)
     if procs <= 1:
         t0 = time.perf_counter()
         T.modified_weights(W, cfg["n"], cluster_range=(cb, T.nclusters), out=F)
-        t_w = (time.perf_counter() - t0) * tot / acc if acc > 0 else 0.0
+        t_w_raw = time.perf_counter() - t0
         if fhat is None:
             F = T.modified_weights(W, cfg["n"], cluster_range=(1, T.nclusters), out=F)
         t0 = time.perf_counter()
         T.treecode(cfg["kernel"], cfg["eps"], cfg["n"], cfg["theta"], W, fhat=F, targets=tg)
-        t_e = (time.perf_counter() - t0) * N / len(tg)
+        t_e_raw = time.perf_counter() - t0
     else:
         import multiprocessing as mp
         if fhat is None:
@@ -170,16 +183,19 @@ def oracle_sample(cfg, X, W, S_targets, weight_frac=0.1, seed=1, fhat=None, proc
         cuts = [cb + int(np.searchsorted(cum, cum[-1] * r / procs)) for r in range(procs)] + [T.nclusters]
         wr = [(b, e) for b, e in zip(cuts[:-1], cuts[1:]) if e > b]   # cluster ranges balanced by N_C
         with mp.get_context("fork").Pool(procs) as pool:
-            t_w = (max(pool.map(_orc_weights, wr)) * tot / acc) if (acc > 0 and wr) else 0.0
-            t_e = max(pool.map(_orc_eval, np.array_split(tg, procs))) * N / len(tg)
+            t_w_raw = max(pool.map(_orc_weights, wr)) if (acc > 0 and wr) else 0.0
+            t_e_raw = max(pool.map(_orc_eval, np.array_split(tg, procs)))
         _ORC.clear()
+    t_w, t_e = t_w_raw * w_scale, t_e_raw * e_scale
     total = t_tree + t_w + t_e
-    return N / total, dict(t_tree_s=t_tree, t_weights_s_extrapolated=t_w, t_eval_s_extrapolated=t_e,
+    return N / total, dict(t_tree_s=t_tree, t_weights_sample_s=t_w_raw, weights_scale=w_scale,
+                           t_weights_s_extrapolated=t_w, t_eval_sample_s=t_e_raw, eval_scale=e_scale,
+                           t_eval_s_extrapolated=t_e, sample_wall_s=t_tree + t_w_raw + t_e_raw,
                            weight_clusters=int(T.nclusters - cb), eval_targets=int(len(tg)),
                            processes=procs), F
 
 
-def run_reference(args, cfg, rank):
+def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
     X, W = KI.config_particles(args.config)
@@ -189,25 +205,51 @@ def run_reference(args, cfg, rank):
     _, _, F = oracle_sample(cfg, X, W, 50, weight_frac=0.0)
     procs = host_cores()
     S = 100 * procs
-    times = []
+    times, dets = [], []
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
         v, det, _ = oracle_sample(cfg, X, W, S, seed=100 + i, fhat=F, procs=procs)
         if i >= args.warmup:
             times.append(cfg["N"] / v)
+            dets.append(det)
     tstep = sum(times) / len(times)
     val = cfg["N"] / tstep
+    measured = {k: sum(d[k] for d in dets) / len(dets) for k in
+                ("t_tree_s", "t_weights_sample_s", "weights_scale", "t_eval_sample_s", "eval_scale", "sample_wall_s")}
     sample = (f"per step: full oracle tree build (1 process); Algorithm 1 on the last clusters holding >=10% of "
               f"sum N_C (time x sum N_C ratio) and Algorithm 2 on {S} random targets (time x N/{S}), both split "
               f"over {procs} processes of the single-threaded oracle (slowest process timed)")
-    line = {"impl": "reference", "metric": metric_for(args.config), "value": val, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tstep * 1e3,
+    line = {"impl": "reference", "metric": metric_for(args.config), "value": val, "unit": UNIT,
+            "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup, "ms_per_step": tstep * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (kitc_inputs, seed 0)",
-            "config": {"workload": f"{args.config}: " + json.dumps(cfg), "sample": sample},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": "oracle", "sample": sample},
+            "precision": "fp64, long double per-target accumulators (the CPU oracle, oracle/kitc_oracle.c)",
+            "data": data_str(cfg), "config": {"workload": workload(args.config)},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": procs, "kind": "oracle", "sample": sample,
+                             "measured_per_step": measured,
+                             "note": "time per step = t_tree + t_weights_sample x weights_scale + "
+                                     "t_eval_sample x eval_scale (extrapolated; sample_wall_s is what ran)"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def data_str(cfg):
+    return "synthetic (kitc_inputs: " + (
+        "organism pairs of the paper's Example 1, unit forces +-t" if cfg["geometry"] == "organisms"
+        else f"{cfg['geometry']}, weights uniform [-1,1]^m") + ", seed 0)"
+
+
+def probe_fp64_peak(seconds=0.5):
+    """DFMA rate measured on this box (tools/libfp64_peak.so, untimed, before the timed region)."""
+    import ctypes as Cc
+    try:
+        L = Cc.CDLL(os.path.join(ROOT, "tools", "libfp64_peak.so"))
+        L.kitc_probe_dfma_tflops.argtypes = [Cc.c_double, Cc.POINTER(Cc.c_double), Cc.POINTER(Cc.c_double)]
+        tf, fc = Cc.c_double(), Cc.c_double()
+        if L.kitc_probe_dfma_tflops(seconds, Cc.byref(tf), Cc.byref(fc)) != 0:
+            return None
+        return {"tflops": tf.value, "fma_per_sm_clk_at_max_clock": fc.value,
+                "how": f"tools/fp64_peak.cu: 148 SMs x 4 CTAs x 256 threads, 8 independent DFMA chains, {seconds} s"}
+    except OSError:
+        return None
 
 
 # ----------------------------------------------------------------------------- GPU leg
@@ -252,7 +294,7 @@ def run_kitc(args, cfg, rank, world, local_rank):
         dist.all_reduce(hi, op=dist.ReduceOp.MAX)
         if not torch.equal(lo, hi):
             raise RuntimeError("ranks built different trees")
-    cshards = D.cluster_shards(rg["begin"], rg["end"], world, skip_root=True)
+    cshards = D.cluster_shards(rg["begin"], rg["end"], world, skip_root=True)   # targets = sources, theta < 1 (A16)
     S = D.padded_shard_size(cshards)
     cb, ce = cshards[rank]
     L = kitc.kitc_fhat_cluster_len(kern, n)
@@ -390,6 +432,7 @@ def run_kitc(args, cfg, rank, world, local_rank):
         ref = kitc.direct(Xd, Wd, kern, eps)
         check = {"E_vs_gpu_direct": kitc.rel_error(ref, out)}
 
+    probe = probe_fp64_peak() if rank == 0 else None
     if rank != 0:
         return
     peaks = {}
@@ -401,46 +444,93 @@ def run_kitc(args, cfg, rank, world, local_rank):
     peak_tflops = PEAK_SMS * PEAK_FMA_PER_CLK * 2 * smax * 1e6 / 1e12
     achieved = flops_eval / (eval_launch_ms * 1e-3) / 1e12
     traffic, traffic_src = None, None
+    from paper_1902_02250_b200 import build as B
+    bid = B.build_id()
+    traffic_build = None
     try:  # dram read + write bytes of one k_eval launch from the committed ncu --set full capture
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[args.config]
-        traffic, traffic_src = tr["dram_bytes_per_launch"], tr["source"]
+        traffic, traffic_src, traffic_build = tr["dram_bytes_per_launch"], tr["source"], tr.get("build_id")
     except Exception:
         pass
     roof = {"bound": "alu", "kernel": "k_eval (treecode evaluation)", "achieved": achieved,
             "peak": peak_tflops, "unit": "TFLOP/s", "frac": achieved / peak_tflops, "traffic": traffic,
             "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
-            "traffic_source": traffic_src,
-            "peak_source": f"derived: {PEAK_SMS} SMs x {PEAK_FMA_PER_CLK} FP64 FMA/clk x 2 x {smax:.0f} MHz "
-                           "(DFMA probe measured 34.1 TFLOP/s, profiles/r01_fp64_peak.txt)",
+            "traffic_source": traffic_src, "build_id": bid, "traffic_build_id": traffic_build,
+            "traffic_same_build": traffic_build == bid,
+            "peak_source": f"derived (contract: ALU-bound peak from unit counts and clocks): {PEAK_SMS} SMs x "
+                           f"{PEAK_FMA_PER_CLK} FP64 FMA/clk x 2 x {smax:.0f} MHz",
+            "peak_measured": probe["tflops"] if probe else None,
+            "frac_of_measured": (achieved / probe["tflops"]) if probe else None,
+            "peak_measured_source": probe,
             "algorithmic_flops_per_launch": flops_eval, "pairs_per_launch": pairs,
             "flops_per_pair": FLOPS_PER_PAIR[kern], "launch_ms": eval_launch_ms,
             "step_share": eval_launch_ms / ms_step}
     line = {"metric": metric_for(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (kitc_inputs: " + (
-                "organism pairs of the paper's Example 1, unit forces +-t" if cfg["geometry"] == "organisms"
-                else f"{cfg['geometry']}, weights uniform [-1,1]^m") + ", seed 0)",
-            "config": {"workload": f"{args.config} ({KI.CONFIGS[args.config]})",
-                       "parallelism": f"tree replicated, fhat sharded, targets dp{world} (64-batch chunks interleaved)",
-                       "fhat_exchange": exchange,
-                       "l2": "flushed between timed steps (256 MB write, untimed)",
-                       "clusters": C, "depth": T.depth, "batches": T.nbatches},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "precision": PRECISION,
+            "data": data_str(cfg),
+            "config": {"workload": workload(args.config)},
+            "setup": {"parallelism": f"tree replicated, fhat sharded, targets dp{world} (64-batch chunks interleaved)",
+                      "fhat_exchange": exchange,
+                      "l2": "flushed between timed steps (256 MB write, untimed)",
+                      "clusters": C, "depth": T.depth, "batches": T.nbatches},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "check": check}
     print(json.dumps(line), flush=True)
 
 
+def launch_ranks(args):
+    """--gpus N > 1 without a torch.distributed environment: re-run this command under
+    torch.distributed.run, one process per GPU (127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")           # communicator lines (rank count) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, rank, world):
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        t = torch.ones(1, device="cuda" if torch.cuda.is_available() else "cpu")
+        dist.all_reduce(t)
+        seen = int(t.item())
+        dist.destroy_process_group()
+    else:
+        seen = 1
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": seen, "gpus_arg": args.gpus}), flush=True)
+
+
 def main():
     args = parse()
     cfg = dict(KI.CONFIGS[args.config])
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        sys.exit(launch_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, cfg, rank)
+        run_reference(args, cfg, rank, world)
+        return
+    if world != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: one rank per GPU is required")
+    if args.dry_run:
+        dry_run(args, rank, world)
         return
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # communicator init lines show the rank count
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        import torch
+        if torch.cuda.device_count() < world:
+            sys.exit(f"bench.py: --gpus {world} but this node has {torch.cuda.device_count()} GPUs")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)

@@ -18,10 +18,13 @@
  *
  * Conventions (all entry points):
  *  - Pointers named *_dev are CUDA device pointers; *_host are host pointers.
- *    The CALLER owns every buffer passed in.  A kitc_tree handle owns the
- *    device memory of the tree it holds (allocated stream-ordered from the
- *    device's default memory pool on the stream of kitc_build_tree, retained
- *    and reused across rebuilds, released by kitc_tree_free).
+ *    The CALLER owns every buffer passed in.  The device memory of a tree
+ *    handle comes from the caller's kitc_allocator (kitc_tree_create_with_
+ *    allocator; the Python binding passes PyTorch's caching allocator), or, for
+ *    kitc_tree_create, from cudaMallocAsync on the device's default pool (whose
+ *    attributes the library never changes).  It is requested on the stream of
+ *    the call that needs it, retained across rebuilds (reallocated only to
+ *    grow) and released by kitc_tree_free.  kitc_tree_workspace_bytes bounds it.
  *  - Layouts: coordinates are AoS double[N][3]; weights are AoS double[N][m];
  *    outputs are AoS double[N][p]; all in the caller's ORIGINAL particle order.
  *  - Work is enqueued on the caller's stream `s` (cudaStream_t passed as void*;
@@ -77,7 +80,24 @@ kitc_status kitc_kernel_dims(int32_t kernel, int32_t* m, int32_t* p);
  * EINVAL for unknown k or n out of range. */
 kitc_status kitc_fhat_cluster_len(int32_t kernel, int32_t n, int64_t* len);
 
-/* Create an empty tree handle (no device memory yet).  *out = NULL on error. */
+/* Device-memory provider of a tree handle (device memory is
+ * the caller's).  alloc(bytes, stream, ctx) returns a 16-byte aligned device
+ * pointer usable in stream order on `stream` (a cudaStream_t as void*), or NULL
+ * (-> KITC_ENOMEM); release(ptr, stream, ctx) gives it back once the work
+ * enqueued on `stream` is done with it.  Called from inside kitc_build_tree,
+ * kitc_modified_weights, kitc_eval_targets (growth only) and kitc_tree_free. */
+typedef struct {
+    void* (*alloc)(size_t bytes, void* stream, void* ctx);
+    void (*release)(void* ptr, void* stream, void* ctx);
+    void* ctx;
+} kitc_allocator;
+
+/* Create an empty tree handle (no device memory yet) whose device memory comes
+ * from *a (copied; NULL = cudaMallocAsync).  EINVAL if a has a NULL member.
+ * *out = NULL on error. */
+kitc_status kitc_tree_create_with_allocator(const kitc_allocator* a, kitc_tree** out);
+
+/* kitc_tree_create_with_allocator(NULL, out). */
 kitc_status kitc_tree_create(kitc_tree** out);
 
 /* Build the cluster tree of N particles (Algorithm 2 line 5; rule
@@ -229,12 +249,18 @@ kitc_status kitc_direct_sample(int32_t kernel, double eps, int32_t self, const i
                                void* s);
 
 /* Relative error E (Eq. error) of approx vs ref, both device
- * double[count] (rows of p components concatenated).  Writes E to
- * *E_host (synchronizes).  EINVAL if the reference is identically zero. */
+ * double[count] (rows of p components concatenated):
+ *   E = ( sum_i (ref_i - approx_i)^2 / sum_i ref_i^2 )^(1/2).
+ * scratch_dev: caller-owned device double[KITC_REL_ERROR_SCRATCH] (per-block
+ * partial sums; no allocation inside).  Writes E to *E_host (synchronizes the
+ * stream; the partials are added in long double on the host).  EINVAL if the
+ * reference is identically zero, count < 1 or a pointer is NULL. */
+#define KITC_REL_ERROR_SCRATCH 1184
 kitc_status kitc_rel_error(const double* ref_dev, const double* approx_dev, int64_t count,
-                           double* E_host, void* s);
+                           double* scratch_dev, double* E_host, void* s);
 
-/* Free the handle and its device memory (stream-ordered on the build stream). */
+/* Free the handle and its device memory.  Waits for the device (cudaDeviceSynchronize)
+ * first: calls on any stream may still be using the handle's buffers. */
 void kitc_tree_free(kitc_tree* t);
 
 /* Thread-local message for the last non-OK status ("" if none). */

@@ -18,6 +18,17 @@ def sources():
                   [os.path.join(ROOT, "include", "kitc.h")])
 
 
+def build_id() -> str:
+    """sha256 (16 hex) of the library's sources: ties a profile (profiles/ncu_traffic.json)
+    to the build it was captured on."""
+    import hashlib
+    h = hashlib.sha256()
+    for src in sources():
+        with open(src, "rb") as f:
+            h.update(os.path.basename(src).encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
+
+
 def stale() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -54,6 +65,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.check_call(link)
     os.replace(tmp, LIB)
     return LIB
+
+
+PROBE_SRC = os.path.join(ROOT, "tools", "fp64_peak.cu")
+PROBE_LIB = os.path.join(ROOT, "tools", "libfp64_peak.so")
+
+
+def build_probe(force: bool = False) -> str:
+    """tools/libfp64_peak.so: the DFMA-rate probe bench.py reports beside the derived
+    FP64 peak (measurement tool, not part of libkitc)."""
+    if not force and os.path.exists(PROBE_LIB) and os.path.getmtime(PROBE_LIB) >= os.path.getmtime(PROBE_SRC):
+        return PROBE_LIB
+    nvcc = os.environ.get("NVCC", "nvcc")
+    if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
+        nvcc = "/usr/local/cuda/bin/nvcc"
+    subprocess.check_call([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-DKITC_PROBE_LIB",
+                           "-Xcompiler", "-fPIC", "-shared", "-o", PROBE_LIB, PROBE_SRC])
+    return PROBE_LIB
 
 
 if __name__ == "__main__":

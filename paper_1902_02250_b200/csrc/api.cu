@@ -40,10 +40,20 @@ kitc_status kitc_kernel_dims(int32_t kernel, int32_t* m, int32_t* p) {
     return KITC_OK;
 }
 
-kitc_status kitc_tree_create(kitc_tree** out) {
+kitc_status kitc_tree_create(kitc_tree** out) { return kitc_tree_create_with_allocator(nullptr, out); }
+
+kitc_status kitc_tree_create_with_allocator(const kitc_allocator* a, kitc_tree** out) {
     if (!out) return set_error(KITC_EINVAL, "kitc_tree_create: out is NULL");
     *out = nullptr;
-    KITC_GUARD(*out = new kitc_tree(); return KITC_OK;)
+    if (a && (!a->alloc || !a->release))
+        return set_error(KITC_EINVAL, "kitc_tree_create_with_allocator: alloc and release are both required");
+    KITC_GUARD({
+        kitc_tree* t = new kitc_tree();
+        if (a) t->allocator = *a;
+        t->for_each_buf([t](DevBuf& b) { b.al = &t->allocator; });
+        *out = t;
+        return KITC_OK;
+    })
 }
 
 kitc_status kitc_build_tree(kitc_tree* t, const double* xyz, int64_t N, int32_t N0, void* s) {
@@ -176,18 +186,17 @@ kitc_status kitc_direct_sample(int32_t kernel, double eps, int32_t self, const i
     KITC_GUARD(return direct(kernel, eps, self, xs, nt, xs, ws, Ns, out, (cudaStream_t)s, idx);)
 }
 
-kitc_status kitc_rel_error(const double* ref, const double* ap, int64_t n, double* E, void* s) {
-    KITC_GUARD(return rel_error(ref, ap, n, E, (cudaStream_t)s);)
+kitc_status kitc_rel_error(const double* ref, const double* ap, int64_t n, double* scratch, double* E, void* s) {
+    KITC_GUARD(return rel_error(ref, ap, n, scratch, E, (cudaStream_t)s);)
 }
 
 void kitc_tree_free(kitc_tree* t) {
     if (!t) return;
+    // calls on other streams may still use the handle's buffers: wait for the whole
+    // device before releasing them (freeing is rare; correctness over latency)
+    cudaDeviceSynchronize();
     cudaStream_t s = t->stream;
-    for (DevBuf* b : {&t->x, &t->y, &t->z, &t->perm, &t->x2, &t->y2, &t->z2, &t->perm2, &t->w, &t->src, &t->box, &t->cr,
-                      &t->topo, &t->grid, &t->tord, &t->leaves, &t->bstart, &t->bcount, &t->d_items, &t->d_part, &t->d_cnt, &t->d_off,
-                      &t->d_lvl, &t->d_split, &t->d_flag, &t->d_witems, &t->d_wpart, &t->d_tkey, &t->d_tkey2,
-                      &t->d_tidx, &t->d_tidx2, &t->d_txyz, &t->d_tcub, &t->d_tbox})
-        b->release(s);
+    t->for_each_buf([s](DevBuf& b) { b.release(s); });
     if (t->ev_stage) cudaEventDestroy(t->ev_stage);
     t->h_stage.release();
     t->h_cnt.release();

@@ -24,35 +24,36 @@ kitc_status check_cuda(cudaError_t e, const char* what) {
     return set_error(KITC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// Keep freed pool memory cached so per-step rebuilds do not return memory to
-// the driver (stream-ordered allocator, default pool of the current device).
-static void retain_pool() {
-    static thread_local int done_dev = -1;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done_dev = dev;
-}
-
+// Buffers are retained by their handle across rebuilds and only reallocated when
+// they must grow (by 25% + 256 B), so steady-state steps allocate nothing.
 kitc_status DevBuf::ensure(size_t need, cudaStream_t s, bool keep) {
     if (need <= bytes) return KITC_OK;
-    retain_pool();
-    size_t nb = need + need / 4 + 256;
+    size_t nb = (need + need / 4 + 256 + 255) / 256 * 256;
     void* np = nullptr;
-    KITC_CUDA(cudaMallocAsync(&np, nb, s));
+    if (al && al->alloc) {
+        np = al->alloc(nb, (void*)s, al->ctx);
+        if (!np) return set_error(KITC_ENOMEM, "kitc_allocator: allocation of " + std::to_string(nb) + " bytes failed");
+        if (reinterpret_cast<uintptr_t>(np) % 16) {
+            al->release(np, (void*)s, al->ctx);
+            return set_error(KITC_EINVAL, "kitc_allocator: pointer not 16-byte aligned");
+        }
+    } else {
+        KITC_CUDA(cudaMallocAsync(&np, nb, s));
+    }
     if (keep && p && bytes) KITC_CUDA(cudaMemcpyAsync(np, p, bytes, cudaMemcpyDeviceToDevice, s));
-    if (p) KITC_CUDA(cudaFreeAsync(p, s));
+    release(s);
     p = np;
     bytes = nb;
     return KITC_OK;
 }
 
 void DevBuf::release(cudaStream_t s) {
-    if (p) cudaFreeAsync(p, s);
+    if (p) {
+        if (al && al->alloc)
+            al->release(p, (void*)s, al->ctx);
+        else
+            cudaFreeAsync(p, s);
+    }
     p = nullptr;
     bytes = 0;
 }

@@ -178,15 +178,15 @@ kitc_status direct(int kernel, double eps, int self, const double* xt, int64_t N
     return KITC_OK;
 }
 
-kitc_status rel_error(const double* ref, const double* ap, int64_t n, double* E, cudaStream_t s) {
+static_assert(2 * kErrBlocks == KITC_REL_ERROR_SCRATCH, "include/kitc.h KITC_REL_ERROR_SCRATCH");
+
+kitc_status rel_error(const double* ref, const double* ap, int64_t n, double* part, double* E, cudaStream_t s) {
     if (!ref || !ap || !E || n < 1) return set_error(KITC_EINVAL, "kitc_rel_error: bad arguments");
-    double* part = nullptr;
-    KITC_CUDA(cudaMallocAsync(&part, 2 * kErrBlocks * sizeof(double), s));
+    if (!part) return set_error(KITC_EINVAL, "kitc_rel_error: NULL scratch");
     k_relerr<<<kErrBlocks, 256, 0, s>>>(ref, ap, n, part); note_launch();
+    KITC_CUDA(cudaGetLastError());
     std::vector<double> h(2 * kErrBlocks);
-    cudaError_t e1 = cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s);
-    cudaFreeAsync(part, s);
-    KITC_CUDA(e1);
+    KITC_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
     KITC_CUDA(cudaStreamSynchronize(s));
     long double num = 0.0L, den = 0.0L;
     for (int b = 0; b < kErrBlocks; ++b) {

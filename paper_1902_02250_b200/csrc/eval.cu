@@ -185,6 +185,9 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
                   ws.bar + (k & 1));
     };
     if (leader) {
+        // the buffers were last read through the generic proxy (previous cluster): order
+        // those reads before the async-proxy (bulk copy) writes, as for the refills below
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(0, base);
         if (NS > 1) issue(1, base + 1);
     }
@@ -409,6 +412,7 @@ __device__ __forceinline__ void far_field_team(double x, double y, double z, con
                   ws.bar + (k & 1));
     };
     if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // as in far_field
         issue(0, base);
         if (NS > 1) issue(1, base + 1);
     }

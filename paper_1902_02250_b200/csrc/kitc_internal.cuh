@@ -38,10 +38,14 @@ kitc_status check_cuda(cudaError_t e, const char* what);
     } while (0)
 #define KITC_CUDA(expr) KITC_TRY(::kitc::check_cuda((expr), #expr))
 
-// Stream-ordered device buffer, grown on demand, retained across rebuilds.
+// Stream-ordered device buffer, grown on demand, retained across rebuilds.  Memory
+// comes from the handle's kitc_allocator (include/kitc.h) when it has one (the
+// Python binding passes torch's caching allocator), else cudaMallocAsync from the
+// device's default pool (its attributes are left untouched).
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    const kitc_allocator* al = nullptr;  // the owning handle's provider (nullptr: cudaMallocAsync)
     kitc_status ensure(size_t need, cudaStream_t s, bool keep = false);
     void release(cudaStream_t s);
     template <class T> T* as() const { return static_cast<T*>(p); }
@@ -104,6 +108,16 @@ struct kitc_tree {
     // separate-target scratch (kitc_eval_targets): Morton keys / indices (double
     // buffers for the radix sort), sorted coordinates, cub temp, bounding box
     mutable kitc::DevBuf d_tkey, d_tkey2, d_tidx, d_tidx2, d_txyz, d_tcub, d_tbox;
+
+    // device-memory provider (include/kitc.h kitc_allocator); alloc == NULL: cudaMallocAsync
+    kitc_allocator allocator{};
+    template <class F> void for_each_buf(F&& f) {
+        for (kitc::DevBuf* b : {&x, &y, &z, &perm, &x2, &y2, &z2, &perm2, &w, &src, &box, &cr, &topo, &grid, &tord,
+                                &leaves, &bstart, &bcount, &d_items, &d_part, &d_cnt, &d_off, &d_lvl, &d_split,
+                                &d_flag, &d_witems, &d_wpart, &d_tkey, &d_tkey2, &d_tidx, &d_tidx2, &d_txyz,
+                                &d_tcub, &d_tbox})
+            f(*b);
+    }
 };
 
 namespace kitc {
@@ -133,6 +147,6 @@ kitc_status eval_targets(const kitc_tree* t, int kernel, int n, double theta, do
 kitc_status direct(int kernel, double eps, int self, const double* xt, int64_t Nt,
                    const double* xs, const double* ws, int64_t Ns, double* out, cudaStream_t s,
                    const int64_t* tidx = nullptr);
-kitc_status rel_error(const double* ref, const double* approx, int64_t count, double* E,
+kitc_status rel_error(const double* ref, const double* approx, int64_t count, double* scratch, double* E,
                       cudaStream_t s);
 }  // namespace kitc

@@ -11,8 +11,9 @@ Decomposition (DESIGN.md "Multi-GPU"):
     by two device-side barriers (PeerFhat).  The baseline exchange -- an NCCL
     all-gather of padded shards placed at their cluster offsets
     (all_gather_fhat) -- stays available and is the bench's cross-check;
-  * targets are partitioned by warp batches (<= 4 targets of one leaf), contiguous ranges balanced
-    by target count; outputs stay sharded (each rank writes its targets).
+  * targets are partitioned by warp batches (<= 4 targets of one leaf): chunks of 64 batches
+    dealt round-robin to the ranks (kitc_eval_part), so every rank samples the whole domain;
+    outputs stay sharded (each rank writes its targets).
 Per-target traversal and summation orders do not depend on the partition, so
 outputs are bitwise identical for any number of ranks.
 """
@@ -36,10 +37,12 @@ def balanced_ranges(weights, k, start=0):
     return [(cuts[i], cuts[i + 1]) for i in range(k)]
 
 
-def cluster_shards(begin, end, k, skip_root=True):
-    """Cluster ranges per rank, balanced by N_C.  skip_root: with targets =
-    sources and theta < 1 the root is never accepted (every target lies in
-    its box, R <= r), so its fhat is never read (reading A16)."""
+def cluster_shards(begin, end, k, skip_root=False):
+    """Cluster ranges per rank, balanced by N_C.  skip_root=True is valid ONLY
+    for targets = sources with theta < 1: then the root is never accepted
+    (every target lies in its box, R <= r), so its fhat is never read
+    (reading A16).  Separate targets (kitc_eval_targets) may accept
+    the root: keep the default."""
     sizes = np.asarray(end) - np.asarray(begin)
     return balanced_ranges(sizes, k, start=1 if (skip_root and len(sizes) > 1) else 0)
 
@@ -88,9 +91,14 @@ class PeerFhat:
         assert self.ptrs[self.hdl.rank] == self.fhat.data_ptr(), "symmetric memory: unexpected local mapping"
 
     def modified_weights(self, T, kernel, n, W, cluster_range, stream=None):
+        """All three steps are enqueued on `stream` (default: the current stream), so the
+        barriers bracket the peer-store kernel whatever stream the caller uses."""
+        import torch
         from . import kitc
         cb, ce = cluster_range
-        self.hdl.barrier(channel=0)   # no rank still reads the previous step's fhat
-        kitc.kitc_modified_weights_peers(T.handle, kernel, n, kitc._ptr(W), cb, ce, self.ptrs, kitc._stream(stream))
-        self.hdl.barrier(channel=1)   # every replica complete
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.hdl.barrier(channel=0)   # no rank still reads the previous step's fhat
+            kitc.kitc_modified_weights_peers(T.handle, kernel, n, kitc._ptr(W), cb, ce, self.ptrs, kitc._stream(s))
+            self.hdl.barrier(channel=1)   # every replica complete
         return self.fhat

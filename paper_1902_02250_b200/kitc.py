@@ -28,7 +28,8 @@ EVAL_SIZE_CHECK = 1   # kitc_eval_flag (include/kitc.h)
 KERNELS = {"stokeslet": STOKESLET, "rotlet": ROTLET, "stokeslet_rotlet": STOKESLET_ROTLET}
 
 # every symbol include/kitc.h declares
-EXPORTS = ("kitc_kernel_dims", "kitc_fhat_cluster_len", "kitc_tree_create", "kitc_build_tree", "kitc_tree_info",
+EXPORTS = ("kitc_kernel_dims", "kitc_fhat_cluster_len", "kitc_tree_create", "kitc_tree_create_with_allocator",
+           "kitc_build_tree", "kitc_tree_info",
            "kitc_tree_export", "kitc_modified_weights", "kitc_modified_weights_peers", "kitc_eval", "kitc_eval_ex", "kitc_eval_part", "kitc_eval_targets", "kitc_eval_targets_ex", "kitc_batch_targets",
            "kitc_direct", "kitc_direct_sample", "kitc_rel_error", "kitc_tree_free", "kitc_last_error",
            "kitc_launch_count")
@@ -40,6 +41,30 @@ class KitcError(RuntimeError):
         self.status = status
 
 
+# kitc_allocator (include/kitc.h): device memory of tree handles from PyTorch's caching allocator
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_RELEASE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class KitcAllocator(C.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("release", _RELEASE_FN), ("ctx", C.c_void_p)]
+
+
+def _torch_alloc(nbytes, stream, ctx):
+    try:
+        return torch.cuda.caching_allocator_alloc(int(nbytes), stream=int(stream or 0))
+    except Exception:   # out of memory -> NULL -> KITC_ENOMEM
+        return None
+
+
+def _torch_release(ptr, stream, ctx):
+    torch.cuda.caching_allocator_delete(int(ptr))
+
+
+TORCH_ALLOCATOR = KitcAllocator(_ALLOC_FN(_torch_alloc), _RELEASE_FN(_torch_release), None)
+REL_ERROR_SCRATCH = 1184   # KITC_REL_ERROR_SCRATCH
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libkitc.so not built ({LIB_PATH}); run __graft_entry__.build()")
@@ -49,6 +74,7 @@ def _load():
     sig = {
         "kitc_kernel_dims": [i32, P(i32), P(i32)],
         "kitc_tree_create": [P(vp)],
+        "kitc_tree_create_with_allocator": [P(KitcAllocator), P(vp)],
         "kitc_build_tree": [vp, vp, i64, i32, vp],
         "kitc_tree_info": [vp, P(i64), P(i32), P(i64), P(i32)],
         "kitc_tree_export": [vp] + [vp] * 9,
@@ -63,7 +89,7 @@ def _load():
         "kitc_batch_targets": [vp, i64, P(i64)],
         "kitc_direct": [i32, d, i32, vp, i64, vp, vp, i64, vp, vp],
         "kitc_direct_sample": [i32, d, i32, vp, i64, vp, vp, i64, vp, vp],
-        "kitc_rel_error": [vp, vp, i64, P(d), vp],
+        "kitc_rel_error": [vp, vp, i64, vp, P(d), vp],
         "kitc_tree_free": [vp],
         "kitc_last_error": [],
         "kitc_launch_count": [],
@@ -140,6 +166,13 @@ def kitc_tree_create():
     return h
 
 
+def kitc_tree_create_with_allocator(allocator=None):
+    """allocator: a KitcAllocator (default: PyTorch's caching allocator)."""
+    h = C.c_void_p()
+    _call("kitc_tree_create_with_allocator", C.byref(allocator or TORCH_ALLOCATOR), C.byref(h))
+    return h
+
+
 def kitc_build_tree(t, xyz_ptr, N, N0, stream_ptr):
     return _call("kitc_build_tree", t, xyz_ptr, int(N), int(N0), stream_ptr)
 
@@ -197,9 +230,9 @@ def kitc_direct(kernel, eps, self_mode, xt_ptr, Nt, xs_ptr, ws_ptr, Ns, out_ptr,
                  ws_ptr, int(Ns), out_ptr, stream_ptr)
 
 
-def kitc_rel_error(ref_ptr, approx_ptr, count, stream_ptr):
+def kitc_rel_error(ref_ptr, approx_ptr, count, scratch_ptr, stream_ptr):
     E = C.c_double()
-    _call("kitc_rel_error", ref_ptr, approx_ptr, int(count), C.byref(E), stream_ptr)
+    _call("kitc_rel_error", ref_ptr, approx_ptr, int(count), scratch_ptr, C.byref(E), stream_ptr)
     return E.value
 
 
@@ -214,10 +247,11 @@ def kitc_tree_free(t):
 # ---- torch convenience layer ---------------------------------------------------
 
 class Tree:
-    """A built KITC tree (library-owned device memory) over device particles X[N, 3]."""
+    """A built KITC tree over device particles X[N, 3]; its device memory comes from
+    PyTorch's caching allocator (kitc_tree_create_with_allocator)."""
 
     def __init__(self, X, N0, stream=None):
-        self._h = kitc_tree_create()
+        self._h = kitc_tree_create_with_allocator()
         self.build(X, N0, stream)
 
     def build(self, X, N0, stream=None):
@@ -345,7 +379,8 @@ def direct_sample(X, W, kernel, eps, idx, self_omit=True, out=None, stream=None)
 def rel_error(ref, approx, stream=None):
     """E of Eq. error on the GPU (rows concatenated)."""
     assert ref.shape == approx.shape and ref.is_contiguous() and approx.is_contiguous()
-    return kitc_rel_error(_ptr(ref), _ptr(approx), ref.numel(), _stream(stream))
+    scratch = torch.empty(REL_ERROR_SCRATCH, dtype=torch.float64, device=ref.device)
+    return kitc_rel_error(_ptr(ref), _ptr(approx), ref.numel(), _ptr(scratch), _stream(stream))
 
 
 def treecode(X, W, kernel, n, theta, N0, eps, self_omit=True, stats=False, stream=None, tree=None):

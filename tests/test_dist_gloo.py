@@ -41,8 +41,10 @@ def test_balanced_ranges():
         assert len(r) == k and r[0][0] == 0 and r[-1][1] == len(w)
         assert all(r[i][1] == r[i + 1][0] for i in range(k - 1))
         assert all(b <= e for b, e in r)
+    r = D.cluster_shards(np.array([0, 0, 5, 7]), np.array([10, 5, 7, 10]), 2, skip_root=True)
+    assert r[0][0] == 1                                  # root skipped (reading A16, targets = sources)
     r = D.cluster_shards(np.array([0, 0, 5, 7]), np.array([10, 5, 7, 10]), 2)
-    assert r[0][0] == 1                                  # root skipped (reading A16)
+    assert r[0][0] == 0 and r[-1][1] == 4                # default: every cluster (separate targets may accept the root)
 
 
 def _worker(rank, world, port, F, shards_expect, q):

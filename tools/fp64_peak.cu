@@ -16,6 +16,7 @@ __global__ void dfma_loop(double* out, long iters, double a, double b) {
   for (int c = 0; c < CHAINS; ++c) s += acc[c];
   if (s == 12345.678) out[0] = s;
 }
+#ifndef KITC_PROBE_LIB
 int main(int argc, char** argv) {
   int dev = 0; cudaDeviceProp p; cudaGetDeviceProperties(&p, dev);
   int sms = p.multiProcessorCount;
@@ -45,4 +46,44 @@ int main(int argc, char** argv) {
   }
   cudaError_t e = cudaGetLastError(); printf("err %s\n", cudaGetErrorString(e));
   return 0;
+}
+#endif
+
+// Library form for bench.py (built by __graft_entry__.build() into
+// tools/libfp64_peak.so): the DFMA rate of the box, measured untimed before the
+// bench's timed region and reported beside the derived roofline peak.
+extern "C" int kitc_probe_dfma_tflops(double seconds, double* tflops, double* fma_per_sm_clk) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return -1;
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  const int sms = p.multiProcessorCount, threads = 256, bps = 4, CH = 8;
+  double* out = nullptr;
+  if (cudaMalloc(&out, 8) != cudaSuccess) return -1;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  long iters = 1 << 14;
+  dfma_loop<CH><<<sms * bps, threads>>>(out, iters, 0.999999, 1e-7);  // warm-up + calibration
+  cudaEventRecord(e0);
+  dfma_loop<CH><<<sms * bps, threads>>>(out, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const long it2 = (long)(iters * (seconds * 1e3 / ms));
+  cudaEventRecord(e0);
+  dfma_loop<CH><<<sms * bps, threads>>>(out, it2, 0.999999, 1e-7);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double flops = 2.0 * CH * (double)it2 * threads * sms * bps;
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  if (fma_per_sm_clk) *fma_per_sm_clk = flops / 2 / (ms * 1e-3) / sms / (clk * 1e3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
