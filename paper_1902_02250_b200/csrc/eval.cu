@@ -796,6 +796,13 @@ static void launch(const EvalArgs& a, int grid, size_t smem, cudaStream_t s) {
 
 template <int KER>
 static void dispatch(int P, const EvalArgs& a, int grid, size_t smem, cudaStream_t s) {
+#ifdef KITC_ONLY_P  // tuning builds (tools/build_variant.py): one specialised degree, the rest generic
+    if (P == KITC_ONLY_P)
+        launch<KITC_ONLY_P, KER>(a, grid, smem, s);
+    else
+        launch<0, KER>(a, grid, smem, s);
+    return;
+#endif
     switch (P) {
         case 2: launch<2, KER>(a, grid, smem, s); break;
         case 3: launch<3, KER>(a, grid, smem, s); break;
