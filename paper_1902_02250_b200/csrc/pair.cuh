@@ -1,7 +1,8 @@
 // pair.cuh -- the MRS pair terms on CUDA cores (fp64), §7.
 //
-// With d = x - y, s = |d|^2 + eps^2 and rs = s^{-1/2} (hardware rsqrt seed +
-// Newton, 1 ulp), the scalar functions of Eq. MRS_kernels are
+// With d = x - y, s = |d|^2 + eps^2 and rs = s^{-1/2} (hardware rsqrt seed + one
+// cubic correction, <= ~4 ulp, for the direct sum; seed + one Newton step, relative
+// error < 2e-12, for the treecode evaluation -- reading A19), the scalar functions of Eq. MRS_kernels are
 //   8 pi H1 = (2 eps^2 + r^2) s^{-3/2} = rs + eps^2 rs^3
 //   8 pi H2 = rs^3
 //   8 pi Q  = (5 eps^2 + 2 r^2) s^{-5/2} = 2 rs^3 + 3 eps^2 rs^5
