@@ -55,6 +55,7 @@ def lib():
         L.orc_modified_weights.argtypes = [vp, i32, i32, vp, vp]
         L.orc_modified_weights_range.argtypes = [vp, i32, i32, vp, i64, i64, vp]
         L.orc_modified_weights_box.argtypes = [i64, vp, vp, i32, i32, vp, vp, vp]
+        L.orc_modified_weights_upward.argtypes = [vp, i32, i32, vp, vp]
         L.orc_treecode.argtypes = [vp, i32, d, i32, d, i32, vp, vp, vp, i64, vp, vp]
         L.orc_treecode_ex.argtypes = [vp, i32, d, i32, d, i32, i32, vp, vp, vp, i64, vp, vp]
         L.orc_direct.argtypes = [i32, d, i32, i32, i64, vp, vp, vp, i64, vp]
@@ -155,12 +156,17 @@ class Tree:
             _lib.orc_tree_free(h)
             self._h = None
 
-    def modified_weights(self, W, n, cluster_range=None, out=None):
+    def modified_weights(self, W, n, cluster_range=None, out=None, upward=False):
+        """Algorithm 1 per cluster; upward=True: internal clusters from their children's
+        fhat (orc_modified_weights_upward, not in the paper -- SURVEY §8(f) f4)."""
         W = _f64(W)
         m = W.shape[1]
         P = n + 1
         F = np.zeros((self.nclusters, m, P * P * P)) if out is None else out
-        if cluster_range is None:
+        if upward:
+            assert cluster_range is None
+            assert lib().orc_modified_weights_upward(self._h, n, m, _p(W), _p(F)) == 0
+        elif cluster_range is None:
             assert lib().orc_modified_weights(self._h, n, m, _p(W), _p(F)) == 0
         else:
             cb, ce = cluster_range

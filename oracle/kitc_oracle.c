@@ -483,6 +483,61 @@ int orc_modified_weights_range(const orc_tree* T, int n, int m, const double* w,
     return 0;
 }
 
+/* NOT IN THE PAPER: the modified weights of an internal
+ * cluster from its children's.  Eq. modified_weights defines
+ * fhat_k = sum_j L_k(y_j) f_j; L_k is a tensor product of degree-n polynomials
+ * and a child's fhat reproduces every such moment of its particles
+ * (sum_k' fhat_C,k' q(s_C,k') = sum_{j in C} f_j q(y_j)), so Algorithm 1 applied
+ * to the children's proxy points s_C,k' carrying the charges fhat_C,k' gives the
+ * parent's fhat exactly in exact arithmetic, at a cost independent of N_C
+ * (the cost argument of P:465-469).  Leaves use Algorithm 1 on their particles.
+ * Literal: the children in order, each child's proxies in lexicographic
+ * (k1, k2, k3) order are the "particles" of alg1_cluster on the parent's grid.
+ * Clusters are processed in decreasing BFS id (children before parents). */
+int orc_modified_weights_upward(const orc_tree* T, int n, int m, const double* w, double* fhat)
+{
+    if (n < 1 || n > 60 || m < 1) return -1;
+    int64_t N = T->N;
+    int P = n + 1, P3 = P * P * P;
+    size_t per = (size_t)m * P3;
+    double* fs = (double*)malloc((size_t)N * m * sizeof(double));
+    for (int64_t s = 0; s < N; ++s)
+        for (int c = 0; c < m; ++c) fs[s * m + c] = w[T->perm[s] * m + c];
+    double* py = (double*)malloc((size_t)8 * P3 * 3 * sizeof(double));  /* children's proxy points */
+    double* pf = (double*)malloc((size_t)8 * P3 * m * sizeof(double));  /* and their charges */
+    for (int i = T->nnodes - 1; i >= 0; --i) {
+        const orc_node* C = &T->nodes[i];
+        if (C->nchild == 0) {
+            alg1_cluster(C, n, m, T->xs, fs, fhat + per * i);
+            continue;
+        }
+        int64_t q = 0;
+        for (int ch = 0; ch < C->nchild; ++ch) {
+            const orc_node* K = &T->nodes[C->child[ch]];
+            const double* fk = fhat + per * C->child[ch];
+            double s[3 * 64];
+            cluster_grids(K, n, s);
+            for (int k1 = 0; k1 <= n; ++k1)
+                for (int k2 = 0; k2 <= n; ++k2)
+                    for (int k3 = 0; k3 <= n; ++k3, ++q) {
+                        int idx = (k1 * P + k2) * P + k3;
+                        py[3 * q] = s[k1];
+                        py[3 * q + 1] = s[P + k2];
+                        py[3 * q + 2] = s[2 * P + k3];
+                        for (int c = 0; c < m; ++c) pf[q * m + c] = fk[c * P3 + idx];
+                    }
+        }
+        orc_node proxy = *C;  /* the parent's box, its children's proxies as the particles */
+        proxy.begin = 0;
+        proxy.end = q;
+        alg1_cluster(&proxy, n, m, py, pf, fhat + per * i);
+    }
+    free(py);
+    free(pf);
+    free(fs);
+    return 0;
+}
+
 /* Modified weights of one explicit particle set on an explicit box (for the
  * moment-identity pins): y N x 3, f N x m, box lo/hi -> fhat m x (n+1)^3. */
 int orc_modified_weights_box(int64_t N, const double* y, const double* f, int m, int n,
