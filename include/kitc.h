@@ -108,9 +108,20 @@ kitc_status kitc_tree_create(kitc_tree** out);
  * nonempty groups in ascending code bx|by<<1|bz<<2, stably partitioned; a
  * cluster whose split leaves one nonempty child (or lmax = 0) stays a leaf.
  *  xyz_dev: device, double[N][3], original order, finite (else EINVAL).
- *  N in [1, 2^31 - 1], N0 >= 1.  Rebuilding an existing handle is allowed.
- * Synchronizes the stream (one small device->host read per tree level). */
+ *  N in [1, 2^30 - 1], N0 >= 1.  Rebuilding an existing handle is allowed.
+ * The whole build is ONE cooperative kernel on the device (no host work per
+ * level); the call then reads back a block of counters -- its only
+ * synchronisation of the stream.  EINVAL for a tree deeper than 4000 levels. */
 kitc_status kitc_build_tree(kitc_tree* t, const double* xyz_dev, int64_t N, int32_t N0, void* s);
+
+/* Upper bound of the device memory (bytes) a tree handle requests from its
+ * allocator for N particles at leaf size N0 (kitc_build_tree) and modified
+ * weights of `kernel` at degree n (kitc_modified_weights; kitc_eval needs no
+ * more), assuming the worst-case tree of 2N - 1 clusters.  Lets a caller size
+ * an arena for kitc_tree_create_with_allocator up front.  Excludes the
+ * separate-target scratch of kitc_eval_targets (~44 Nt bytes + radix-sort temp).
+ * EINVAL for N < 1, N0 < 1, unknown kernel, n outside [1, 16]. */
+kitc_status kitc_tree_workspace_bytes(int64_t N, int32_t N0, int32_t kernel, int32_t n, size_t* bytes);
 
 /* Sizes of the built tree.  Any output pointer may be NULL.
  *  n_clusters: number of clusters C (BFS order: by level, then by range start);
@@ -146,10 +157,30 @@ kitc_status kitc_tree_export(const kitc_tree* t, int64_t* perm_host, int64_t* be
  *  as 0.  Only the requested clusters' slices are written (a contiguous byte
  *  range per cluster range).  Also gathers w into the tree's sorted layout and
  *  computes every cluster's grid (both used by kitc_eval).
- *  0 <= cluster_begin <= cluster_end <= C.  ESTATE if no tree is built. */
+ *  0 <= cluster_begin <= cluster_end <= C.  ESTATE if no tree is built.
+ *  Enqueue-only: the work items are generated on the device (no host sync). */
 kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const double* w_dev,
                                   int64_t cluster_begin, int64_t cluster_end, double* fhat_dev,
                                   void* s);
+
+/* Modified-weights variants (flags of kitc_modified_weights_ex). */
+typedef enum {
+    /* Not in the paper (the cost argument of P:465-469): the
+     * fhat of an internal cluster is computed from its children's -- Algorithm 1
+     * applied to the children's proxy points carrying their fhat, done as three 1D
+     * interpolation transforms -- instead of from its N_C particles; leaves use
+     * Algorithm 1.  Exact in exact arithmetic (a child's fhat reproduces every
+     * moment of degree <= n per axis), so it changes results by rounding only
+     * (reading A24); the oracle mirrors it (orc_modified_weights_upward).
+     * Requires cluster_end = C (every child of a computed cluster is computed). */
+    KITC_WEIGHTS_UPWARD = 1
+} kitc_weights_flag;
+
+/* kitc_modified_weights with variant flags (0 = Algorithm 1 for every cluster;
+ * unknown bits -> EINVAL). */
+kitc_status kitc_modified_weights_ex(kitc_tree* t, int32_t kernel, int32_t n, const double* w_dev,
+                                     int64_t cluster_begin, int64_t cluster_end, uint32_t flags,
+                                     double* fhat_dev, void* s);
 
 /* Fused modified weights + replication for the multi-GPU path (SURVEY.md §8(e),
  * §8(f) f3): as kitc_modified_weights, but every computed cluster slice is

@@ -56,6 +56,20 @@ kitc_status kitc_tree_create_with_allocator(const kitc_allocator* a, kitc_tree**
     })
 }
 
+kitc_status kitc_tree_workspace_bytes(int64_t N, int32_t N0, int32_t kernel, int32_t n, size_t* bytes) {
+    if (!bytes) return set_error(KITC_EINVAL, "kitc_tree_workspace_bytes: bytes is NULL");
+    if (N < 1 || N > 0x3fffffffLL || N0 < 1) return set_error(KITC_EINVAL, "kitc_tree_workspace_bytes: bad N or N0");
+    int32_t m = 0;
+    KITC_TRY(kitc_kernel_dims(kernel, &m, nullptr));
+    if (n < 1 || n > kitc::kMaxDegree) return set_error(KITC_EINVAL, "kitc_tree_workspace_bytes: n must be in [1, 16]");
+    // worst case: C <= 2N - 1 clusters (every internal cluster has >= 2 children, every
+    // leaf >= 1 particle), depth < min(N, kMaxLevels)
+    const int64_t C = 2 * N - 1;
+    const int32_t depth = (int32_t)std::min<int64_t>(N, kitc::kMaxLevels);
+    *bytes = tree_bytes(N, C) + weights_bytes(N, C, depth, kernel, n);
+    return KITC_OK;
+}
+
 kitc_status kitc_build_tree(kitc_tree* t, const double* xyz, int64_t N, int32_t N0, void* s) {
     if (!t) return set_error(KITC_EINVAL, "kitc_build_tree: NULL handle");
     KITC_GUARD(return build_tree(t, xyz, N, N0, (cudaStream_t)s);)
@@ -78,6 +92,7 @@ kitc_status kitc_tree_export(const kitc_tree* t, int64_t* perm, int64_t* begin, 
     KITC_GUARD({
         cudaStream_t s = t->stream;
         const int64_t C = t->nclusters, N = t->N;
+        KITC_TRY(ensure_host_topology(t));
         if (perm) {
             std::vector<int> p(N);
             KITC_CUDA(cudaMemcpyAsync(p.data(), t->perm.p, N * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -110,6 +125,12 @@ kitc_status kitc_modified_weights(kitc_tree* t, int32_t kernel, int32_t n, const
                                   int64_t ce, double* fhat, void* s) {
     if (!t) return set_error(KITC_EINVAL, "kitc_modified_weights: NULL handle");
     KITC_GUARD(return modified_weights(t, kernel, n, w, cb, ce, &fhat, 1, (cudaStream_t)s);)
+}
+
+kitc_status kitc_modified_weights_ex(kitc_tree* t, int32_t kernel, int32_t n, const double* w, int64_t cb,
+                                     int64_t ce, uint32_t flags, double* fhat, void* s) {
+    if (!t) return set_error(KITC_EINVAL, "kitc_modified_weights_ex: NULL handle");
+    KITC_GUARD(return modified_weights(t, kernel, n, w, cb, ce, &fhat, 1, (cudaStream_t)s, flags);)
 }
 
 kitc_status kitc_modified_weights_peers(kitc_tree* t, int32_t kernel, int32_t n, const double* w, int64_t cb,
@@ -163,6 +184,7 @@ kitc_status kitc_batch_targets(const kitc_tree* t, int64_t be, int64_t* nt) {
     if (!t || !nt) return set_error(KITC_EINVAL, "kitc_batch_targets: NULL argument");
     if (!t->built) return set_error(KITC_ESTATE, "kitc_batch_targets: tree not built");
     if (be < 0 || be > t->nbatches) return set_error(KITC_EINVAL, "kitc_batch_targets: bad batch index");
+    KITC_TRY(ensure_host_topology(t));
     // batches tile the sorted positions leaf by leaf: batch b of leaf l starts at
     // leaf_begin_l + kBatch (b - boff_l), and that is the number of targets before it
     const auto& bo = t->h_leaf_boff;
@@ -197,9 +219,7 @@ void kitc_tree_free(kitc_tree* t) {
     cudaDeviceSynchronize();
     cudaStream_t s = t->stream;
     t->for_each_buf([s](DevBuf& b) { b.release(s); });
-    if (t->ev_stage) cudaEventDestroy(t->ev_stage);
-    t->h_stage.release();
-    t->h_cnt.release();
+    t->h_ctr.release();
     delete t;
 }
 

@@ -26,9 +26,11 @@ kitc_status check_cuda(cudaError_t e, const char* what) {
 
 // Buffers are retained by their handle across rebuilds and only reallocated when
 // they must grow (by 25% + 256 B), so steady-state steps allocate nothing.
+size_t dev_alloc_bytes(size_t need) { return (need + need / 4 + 256 + 255) / 256 * 256; }
+
 kitc_status DevBuf::ensure(size_t need, cudaStream_t s, bool keep) {
     if (need <= bytes) return KITC_OK;
-    size_t nb = (need + need / 4 + 256 + 255) / 256 * 256;
+    size_t nb = dev_alloc_bytes(need);
     void* np = nullptr;
     if (al && al->alloc) {
         np = al->alloc(nb, (void*)s, al->ctx);

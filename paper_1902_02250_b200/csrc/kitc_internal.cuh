@@ -13,6 +13,7 @@ namespace kitc {
 
 constexpr int kMaxDegree = 16;        // n in [1, 16]
 constexpr int kMaxPeers = 8;          // fhat replicas written by one modified-weights call (GPUs per node)
+constexpr int kMaxLevels = 4000;      // tree levels supported by the device build
 #ifndef KITC_GROUP
 #define KITC_GROUP 8
 #endif
@@ -70,13 +71,15 @@ struct kitc_tree {
     int32_t depth = 0;
     int32_t ndegenerate = 0;
     int64_t nclusters = 0;
+    int64_t nleaves = 0;
     int64_t nbatches = 0;
+    int64_t ccap = 0;                    // cluster-table capacity (grown if a build overflows it)
     bool built = false;
 
     // sorted particles (SoA)
     kitc::DevBuf x, y, z, perm;          // double x3, int32
     kitc::DevBuf x2, y2, z2, perm2;      // partition scratch
-    kitc::DevBuf w;                      // sorted weights, m planes of N doubles
+    kitc::DevBuf w;                      // sorted weights, m planes of N
     int32_t w_m = 0;
     kitc::DevBuf src;                    // packed near-field records (x, y, z, w.., pad), src_ld doubles each
     int32_t src_ld = 0;
@@ -84,26 +87,28 @@ struct kitc_tree {
     int32_t grid_n = -1;                 // degree of the stored grids
     int32_t weights_kernel = -1;
 
-    // clusters
-    kitc::DevBuf box;    // double[C][6]  lo xyz, hi xyz
-    kitc::DevBuf cr;     // double4[C]    centre xyz, r^2
-    kitc::DevBuf topo;   // int4[C]       begin, end, first_child, nchild
-    kitc::DevBuf grid;   // double[C][3][n+1]
-    kitc::DevBuf tord;   // int32[N] targets in Morton order inside each leaf (batching only)
-    kitc::DevBuf leaves; // int4[nleaves] begin, end, cluster id, first batch
-    kitc::DevBuf bstart; // int32[nbatches] first position (in tord) of the batch
-    kitc::DevBuf bcount; // int32[nbatches]
+    // clusters (BFS order, capacity ccap)
+    kitc::DevBuf box;     // double[C][6]  lo xyz, hi xyz
+    kitc::DevBuf cr;      // double4[C]    centre xyz, r^2
+    kitc::DevBuf topo;    // int4[C]       begin, end, first_child (-1: leaf), nchild
+    kitc::DevBuf clevel;  // int[C]
+    kitc::DevBuf cparent; // int[C]        (-1 for the root)
+    kitc::DevBuf grid;    // double[C][3][n+1]
+    kitc::DevBuf tord;    // int32[N] targets in Morton order inside each leaf (batching only)
+    kitc::DevBuf leaves;  // int4[nleaves] begin, end, cluster id, first batch (range order)
+    kitc::DevBuf bstart;  // int32[nbatches] first position (in tord) of the batch
+    kitc::DevBuf bcount;  // int32[nbatches]
 
-    // host mirrors of the topology
-    std::vector<int32_t> h_begin, h_end, h_level, h_parent, h_first, h_nchild;
-    std::vector<int32_t> h_leaf_begin;   // leaves in range order: first sorted position
-    std::vector<int64_t> h_leaf_boff;    // first batch of each leaf (+ total at the end)
-    cudaEvent_t ev_stage = nullptr;      // last build's staging copies (h_stage reuse)
+    // host mirrors of the topology, copied on demand (kitc_tree_export, kitc_batch_targets)
+    mutable bool host_topo = false;
+    mutable std::vector<int32_t> h_begin, h_end, h_level, h_parent, h_first, h_nchild;
+    mutable std::vector<int32_t> h_leaf_begin;   // leaves in range order: first sorted position
+    mutable std::vector<int64_t> h_leaf_boff;    // first batch of each leaf (+ total at the end)
 
-    // build scratch
-    kitc::DevBuf d_items, d_part, d_cnt, d_off, d_lvl, d_split, d_flag;
-    kitc::HostBuf h_stage, h_cnt;
-    // weights scratch
+    // device-build scratch (tree.cu) and its pinned counter block
+    kitc::DevBuf b_split, b_pre, b_kids, b_tot8, b_bpart, b_cnt, b_sub, b_ctr;
+    kitc::HostBuf h_ctr;
+    // weights scratch: device-generated work items, per-chunk partial fhat
     kitc::DevBuf d_witems, d_wpart;
     // separate-target scratch (kitc_eval_targets): Morton keys / indices (double
     // buffers for the radix sort), sorted coordinates, cub temp, bounding box
@@ -112,10 +117,10 @@ struct kitc_tree {
     // device-memory provider (include/kitc.h kitc_allocator); alloc == NULL: cudaMallocAsync
     kitc_allocator allocator{};
     template <class F> void for_each_buf(F&& f) {
-        for (kitc::DevBuf* b : {&x, &y, &z, &perm, &x2, &y2, &z2, &perm2, &w, &src, &box, &cr, &topo, &grid, &tord,
-                                &leaves, &bstart, &bcount, &d_items, &d_part, &d_cnt, &d_off, &d_lvl, &d_split,
-                                &d_flag, &d_witems, &d_wpart, &d_tkey, &d_tkey2, &d_tidx, &d_tidx2, &d_txyz,
-                                &d_tcub, &d_tbox})
+        for (kitc::DevBuf* b : {&x, &y, &z, &perm, &x2, &y2, &z2, &perm2, &w, &src, &box, &cr, &topo, &clevel,
+                                &cparent, &grid, &tord, &leaves, &bstart, &bcount, &b_split, &b_pre, &b_kids,
+                                &b_tot8, &b_bpart, &b_cnt, &b_sub, &b_ctr, &d_witems, &d_wpart, &d_tkey, &d_tkey2,
+                                &d_tidx, &d_tidx2, &d_txyz, &d_tcub, &d_tbox})
             f(*b);
     }
 };
@@ -123,9 +128,16 @@ struct kitc_tree {
 namespace kitc {
 // tree.cu
 kitc_status build_tree(kitc_tree* t, const double* xyz, int64_t N, int32_t N0, cudaStream_t s);
+kitc_status ensure_host_topology(const kitc_tree* t);
+const int* tree_level_starts(const kitc_tree* t);  // device int[depth + 2]: first cluster of each level
+int64_t tree_cluster_cap(int64_t N, int32_t N0);
+size_t tree_bytes(int64_t N, int64_t ccap);
+size_t dev_alloc_bytes(size_t need);  // what DevBuf::ensure requests for `need` bytes
+// weights.cu
+size_t weights_bytes(int64_t N, int64_t C, int32_t depth, int kernel, int n);
 // weights.cu
 kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, int64_t cb,
-                             int64_t ce, double* const* fhat_peers, int npeers, cudaStream_t s);
+                             int64_t ce, double* const* fhat_peers, int npeers, cudaStream_t s, unsigned flags = 0);
 // eval.cu
 // A separate target set, Morton-sorted (targets.cu): coordinates SoA by sorted
 // position, the original row of each, count.  Batches are kBatch consecutive

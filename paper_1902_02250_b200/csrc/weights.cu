@@ -125,11 +125,12 @@ template <int P, int M>
 __global__ void __launch_bounds__((P * P + 31) / 32 * 32, P <= 11 ? KITC_W_MINB : 1) k_weights(
     const WItem* __restrict__ items, const double* __restrict__ x, const double* __restrict__ y,
     const double* __restrict__ z, const double* __restrict__ ws, int N, const double* __restrict__ grid,
-    const Peers fhat, double* __restrict__ part) {
+    const Peers fhat, double* __restrict__ part, const int* __restrict__ nitems) {
     constexpr int P2 = P * P, NT = (P2 + 31) / 32 * 32, R = (P2 + kRows - 1) / kRows;
     constexpr int LEN = R * P * M * kRows;
     __shared__ double sg[3 * P];
     __shared__ double Lx[kTile][P], Ly[kTile][P], Lz[kTile][P], sw[kTile][M];
+    if ((int)blockIdx.x >= *nitems) return;  // grid sized by an upper bound (no host sync)
     const WItem it = items[blockIdx.x];
     const int tid = threadIdx.x;
     for (int i = tid; i < 3 * P; i += NT) sg[i] = grid[(size_t)it.c * 3 * P + i];
@@ -193,7 +194,8 @@ struct RItem {
 
 // fhat[c] = sum of its partial slots in chunk order (deterministic).
 __global__ void k_reduce(const RItem* __restrict__ r, int len, const double* __restrict__ part,
-                         const Peers fhat) {
+                         const Peers fhat, const int* __restrict__ nred) {
+    if ((int)blockIdx.x >= *nred) return;
     const RItem it = r[blockIdx.x];
     for (int i = threadIdx.x; i < len; i += blockDim.x) {
         double s = part[(size_t)it.first_slot * len + i];
@@ -202,20 +204,191 @@ __global__ void k_reduce(const RItem* __restrict__ r, int len, const double* __r
     }
 }
 
+// Work items of clusters [cb, ce) built on the device (one CTA): per cluster
+// nch = ceil(N_C / kChunk) chunks; one chunk writes fhat directly, several write
+// partial slots that k_reduce sums in chunk order.  counts[0] = items, [1] = reduce
+// entries.  Exclusive scans in cluster order (three at once).
+__global__ void __launch_bounds__(1024) k_witems(const int4* __restrict__ topo, int cb, int ce, int leaves_only,
+                                                 WItem* __restrict__ items, RItem* __restrict__ red,
+                                                 int* __restrict__ counts) {
+    __shared__ int3 wsum[33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int3 run = make_int3(0, 0, 0);  // items, slots, reduce entries before this chunk of clusters
+    for (int c0 = cb; c0 < ce; c0 += blockDim.x) {
+        const int c = c0 + threadIdx.x;
+        int4 tp = make_int4(0, 0, 0, 0);
+        int nch = 0;
+        if (c < ce) {
+            tp = topo[c];
+            nch = (leaves_only && tp.w > 0) ? 0 : (tp.y - tp.x + kChunk - 1) / kChunk;
+        }
+        const int3 v = make_int3(nch, nch > 1 ? nch : 0, nch > 1 ? 1 : 0);
+        int3 inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
+                      d = __shfl_up_sync(0xffffffffu, inc.z, o);
+            if (lane >= o) {
+                inc.x += a;
+                inc.y += b;
+                inc.z += d;
+            }
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int3 sacc = make_int3(0, 0, 0);
+            for (int k = 0; k < nw; ++k) {
+                const int3 tt = wsum[k];
+                wsum[k] = sacc;
+                sacc.x += tt.x;
+                sacc.y += tt.y;
+                sacc.z += tt.z;
+            }
+            wsum[32] = sacc;
+        }
+        __syncthreads();
+        if (c < ce) {
+            const int io = run.x + wsum[w].x + inc.x - v.x, so = run.y + wsum[w].y + inc.y - v.y,
+                      ro = run.z + wsum[w].z + inc.z - v.z;
+            for (int q = 0; q < nch; ++q)
+                items[io + q] = WItem{c, tp.x + q * kChunk, min(tp.y, tp.x + (q + 1) * kChunk), nch == 1 ? -1 : so + q};
+            if (nch > 1) red[ro] = RItem{c, so, nch, 0};
+        }
+        run.x += wsum[32].x;
+        run.y += wsum[32].y;
+        run.z += wsum[32].z;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        counts[0] = run.x;
+        counts[1] = run.z;
+    }
+}
+
+// Upward pass (flag KITC_WEIGHTS_UPWARD; not in the paper): the
+// fhat of an internal cluster from its children's.  Algorithm 1 applied to a child's
+// proxy points s_C,k' (charges fhat_C,k') on the parent's grid factorises over the
+// axes: fhat_P[k1 k2 k3] += sum_k' A_x[k1][k1'] A_y[k2][k2'] A_z[k3][k3'] fhat_C[k1' k2' k3'],
+// A_l[kp][kc] = L^P_kp(s_C,l,kc) (the 1D barycentric vector of Algorithm 1 lines 9-17,
+// coincidence flag included), so it runs as three 1D transforms of P^4 FMAs each
+// instead of (n+1)^3 "particles" x (n+1)^3 terms; exact in exact arithmetic (the
+// children's fhat reproduce every moment of degree <= n per axis).  One CTA per
+// internal cluster of one level (children first: the host launches deepest level
+// first); one component at a time in shared memory [F | T | ACC | A | grids].
+template <int P, int M>
+__global__ void __launch_bounds__(256) k_upward(const int4* __restrict__ topo, const int* __restrict__ lstart, int lv,
+                                                int cb, const double* __restrict__ grid, const Peers fhat) {
+    constexpr int P2 = P * P, P3 = P2 * P, R = (P2 + kRows - 1) / kRows, LEN = R * P * M * kRows;
+    extern __shared__ __align__(16) double upw[];
+    double* F = upw;            // child fhat, one component [k1][k2][k3]; then T2
+    double* T = F + P3;         // T1
+    double* ACC = T + P3;       // parent fhat, one component
+    double* A = ACC + P3;       // [3][P][P]
+    double* sP = A + 3 * P2;    // parent grid [3][P]
+    const int tid = threadIdx.x;
+    const int L0 = max(lstart[lv], cb), L1 = lstart[lv + 1];
+    const double* src = fhat.p[0];
+    for (int c = L0 + (int)blockIdx.x; c < L1; c += gridDim.x) {
+        const int4 tp = topo[c];
+        if (tp.w == 0) continue;  // leaves: Algorithm 1 on their particles (k_weights)
+        __syncthreads();
+        for (int i = tid; i < 3 * P; i += blockDim.x) sP[i] = grid[(size_t)c * 3 * P + i];
+        for (int m = 0; m < M; ++m) {
+            for (int i = tid; i < P3; i += blockDim.x) ACC[i] = 0.0;
+            for (int ch = tp.z; ch < tp.z + tp.w; ++ch) {
+                __syncthreads();
+                // A_l[kp][kc] = L^P_kp(s_C,l,kc); the child's fhat component m
+                for (int q = tid; q < 3 * P; q += blockDim.x) {
+                    const int l = q / P, kc = q - l * P;
+                    double Lv[P];
+                    bary<P>(grid[((size_t)ch * 3 + l) * P + kc], sP + l * P, Lv);
+#pragma unroll
+                    for (int kp = 0; kp < P; ++kp) A[(l * P + kp) * P + kc] = Lv[kp];
+                }
+                const double* Fc = src + (size_t)ch * LEN;
+                for (int i = tid; i < P3; i += blockDim.x) {
+                    const int row = i / P, k3 = i - row * P;
+                    F[i] = Fc[(((row / kRows) * P + k3) * M + m) * kRows + row % kRows];
+                }
+                __syncthreads();
+                for (int i = tid; i < P3; i += blockDim.x) {  // T[k1][k2'][k3'] = sum_k1' A_x[k1][k1'] F[k1'][k2'][k3']
+                    const int k1 = i / P2, r = i - k1 * P2;
+                    double v = 0.0;
+#pragma unroll
+                    for (int k = 0; k < P; ++k) v = fma(A[k1 * P + k], F[k * P2 + r], v);
+                    T[i] = v;
+                }
+                __syncthreads();
+                for (int i = tid; i < P3; i += blockDim.x) {  // F[k1][k2][k3'] = sum_k2' A_y[k2][k2'] T[k1][k2'][k3']
+                    const int k1 = i / P2, k2 = (i / P) % P, k3 = i % P;
+                    double v = 0.0;
+#pragma unroll
+                    for (int k = 0; k < P; ++k) v = fma(A[(P + k2) * P + k], T[(k1 * P + k) * P + k3], v);
+                    F[i] = v;
+                }
+                __syncthreads();
+                for (int i = tid; i < P3; i += blockDim.x) {  // ACC[k1][k2][k3] += sum_k3' A_z[k3][k3'] F[k1][k2][k3']
+                    const int r = i / P, k3 = i % P;
+                    double v = ACC[i];
+#pragma unroll
+                    for (int k = 0; k < P; ++k) v = fma(A[(2 * P + k3) * P + k], F[r * P + k], v);
+                    ACC[i] = v;
+                }
+            }
+            __syncthreads();
+            for (int q = 0; q < fhat.n; ++q) {
+                double* dst = fhat.p[q] + (size_t)c * LEN;
+                for (int i = tid; i < P3; i += blockDim.x) {
+                    const int row = i / P, k3 = i - row * P;
+                    dst[(((row / kRows) * P + k3) * M + m) * kRows + row % kRows] = ACC[i];
+                }
+                for (int i = tid; i < (R * kRows - P2) * P; i += blockDim.x) {  // padding rows
+                    const int row = P2 + i / P, k3 = i % P;
+                    dst[(((row / kRows) * P + k3) * M + m) * kRows + row % kRows] = 0.0;
+                }
+            }
+        }
+    }
+}
+
+template <int P, int M>
+static void launch_upward(const kitc_tree* t, const int* lstart, int cb, const Peers& fhat, cudaStream_t s) {
+    const size_t smem = (size_t)(3 * P * P * P + 3 * P * P + 3 * P) * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_upward<P, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int lv = t->depth - 1; lv >= 0; --lv) {  // children before parents
+        k_upward<P, M><<<148 * 4, 256, smem, s>>>(t->topo.as<int4>(), lstart, lv, cb, t->grid.as<double>(), fhat);
+        note_launch();
+    }
+}
+
+template <int M>
+static kitc_status dispatch_upward(int n, const kitc_tree* t, const int* lstart, int cb, const Peers& fhat,
+                                   cudaStream_t s) {
+    switch (n + 1) {
+#define KITC_U(P) \
+    case P: launch_upward<P, M>(t, lstart, cb, fhat, s); break;
+        KITC_U(2) KITC_U(3) KITC_U(4) KITC_U(5) KITC_U(6) KITC_U(7) KITC_U(8) KITC_U(9) KITC_U(10)
+        KITC_U(11) KITC_U(12) KITC_U(13) KITC_U(14) KITC_U(15) KITC_U(16) KITC_U(17)
+#undef KITC_U
+        default: return set_error(KITC_EINVAL, "kitc_modified_weights: n out of range");
+    }
+    return KITC_OK;
+}
+
 template <int P, int M>
 static void launch_weights(int nitems, const WItem* items, const kitc_tree* t, const double* ws,
-                           const double* grid, const Peers& fhat, double* part, cudaStream_t s) {
+                           const double* grid, const Peers& fhat, double* part, const int* counts, cudaStream_t s) {
     constexpr int NT = (P * P + 31) / 32 * 32;
     k_weights<P, M><<<nitems, NT, 0, s>>>(items, t->x.as<double>(), t->y.as<double>(), t->z.as<double>(), ws,
-                                          (int)t->N, grid, fhat, part); note_launch();
+                                          (int)t->N, grid, fhat, part, counts); note_launch();
 }
 
 template <int M>
 static kitc_status dispatch(int n, int nitems, const WItem* items, const kitc_tree* t, const double* ws,
-                            const double* grid, const Peers& fhat, double* part, cudaStream_t s) {
+                            const double* grid, const Peers& fhat, double* part, const int* counts, cudaStream_t s) {
     switch (n + 1) {
 #define KITC_W(P) \
-    case P: launch_weights<P, M>(nitems, items, t, ws, grid, fhat, part, s); break;
+    case P: launch_weights<P, M>(nitems, items, t, ws, grid, fhat, part, counts, s); break;
         KITC_W(2) KITC_W(3) KITC_W(4) KITC_W(5) KITC_W(6) KITC_W(7) KITC_W(8) KITC_W(9) KITC_W(10)
         KITC_W(11) KITC_W(12) KITC_W(13) KITC_W(14) KITC_W(15) KITC_W(16) KITC_W(17)
 #undef KITC_W
@@ -227,7 +400,9 @@ static kitc_status dispatch(int n, int nitems, const WItem* items, const kitc_tr
 }  // namespace
 
 kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, int64_t cb, int64_t ce,
-                             double* const* fhat_peers, int npeers, cudaStream_t s) {
+                             double* const* fhat_peers, int npeers, cudaStream_t s, unsigned flags) {
+    if (flags & ~(unsigned)KITC_WEIGHTS_UPWARD) return set_error(KITC_EINVAL, "kitc_modified_weights: unknown flags");
+    const bool upward = (flags & KITC_WEIGHTS_UPWARD) != 0;
     if (npeers < 1 || npeers > kMaxPeers) return set_error(KITC_EINVAL, "kitc_modified_weights: npeers out of range");
     Peers fhat;
     fhat.n = npeers;
@@ -261,44 +436,49 @@ kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, i
     t->weights_kernel = kernel;
     t->weights_ready = true;
     if (ce == cb) return KITC_OK;
-    // work items
-    std::vector<WItem> items;
-    std::vector<RItem> red;
-    int nslots = 0;
-    for (int64_t c = cb; c < ce; ++c) {
-        const int b = t->h_begin[c], e = t->h_end[c];
-        const int nch = (e - b + kChunk - 1) / kChunk;
-        if (nch == 1) {
-            items.push_back(WItem{(int)c, b, e, -1});
-        } else {
-            red.push_back(RItem{(int)c, nslots, nch, 0});
-            for (int q = 0; q < nch; ++q)
-                items.push_back(WItem{(int)c, b + q * kChunk, std::min(e, b + (q + 1) * kChunk), nslots++});
-        }
-    }
-    const size_t o1 = (items.size() * sizeof(WItem) + 15) / 16 * 16, o2 = o1 + red.size() * sizeof(RItem);
-    // staging buffer reuse: wait for the copies that last read h_stage (not the whole stream)
-    if (t->ev_stage) KITC_CUDA(cudaEventSynchronize(t->ev_stage));
-    KITC_TRY(t->h_stage.ensure(o2));
-    std::copy(items.begin(), items.end(), t->h_stage.as<WItem>());
-    std::copy(red.begin(), red.end(), reinterpret_cast<RItem*>(t->h_stage.as<char>() + o1));
-    KITC_TRY(t->d_witems.ensure(o2, s));
-    KITC_CUDA(cudaMemcpyAsync(t->d_witems.p, t->h_stage.p, o2, cudaMemcpyHostToDevice, s));
-    if (!t->ev_stage) KITC_CUDA(cudaEventCreateWithFlags(&t->ev_stage, cudaEventDisableTiming));
-    KITC_CUDA(cudaEventRecord(t->ev_stage, s));
-    KITC_TRY(t->d_wpart.ensure((size_t)std::max(nslots, 1) * LEN * sizeof(double), s));
-    const WItem* di = t->d_witems.as<WItem>();
+    if (upward && (ce != C || npeers != 1))
+        return set_error(KITC_EINVAL, "kitc_modified_weights: KITC_WEIGHTS_UPWARD needs cluster_end = C (children "
+                                      "in range) and one fhat buffer");
+    // work items on the device; grids sized by upper bounds (items: each particle lies in
+    // depth + 1 clusters, each cluster adds at most one partial chunk) -- no host sync
+    const int64_t ncl = ce - cb;
+    const int64_t ub_items = std::min<int64_t>((int64_t)N * (t->depth + 1) / kChunk + ncl, 0x7fffffff);
+    const size_t o1 = ((size_t)ub_items * sizeof(WItem) + 15) / 16 * 16;
+    const size_t o2 = o1 + ((size_t)ncl * sizeof(RItem) + 15) / 16 * 16;
+    KITC_TRY(t->d_witems.ensure(o2 + 16, s));
+    WItem* di = t->d_witems.as<WItem>();
+    RItem* dr = reinterpret_cast<RItem*>(t->d_witems.as<char>() + o1);
+    int* counts = reinterpret_cast<int*>(t->d_witems.as<char>() + o2);
+    k_witems<<<1, 1024, 0, s>>>(t->topo.as<int4>(), (int)cb, (int)ce, upward ? 1 : 0, di, dr, counts); note_launch();
+    KITC_TRY(t->d_wpart.ensure((size_t)std::max<int64_t>(ub_items, 1) * LEN * sizeof(double), s));
     if (m == 3)
-        KITC_TRY(dispatch<3>(n, (int)items.size(), di, t, t->w.as<double>(), t->grid.as<double>(), fhat,
-                             t->d_wpart.as<double>(), s));
+        KITC_TRY(dispatch<3>(n, (int)ub_items, di, t, t->w.as<double>(), t->grid.as<double>(), fhat,
+                             t->d_wpart.as<double>(), counts, s));
     else
-        KITC_TRY(dispatch<6>(n, (int)items.size(), di, t, t->w.as<double>(), t->grid.as<double>(), fhat,
-                             t->d_wpart.as<double>(), s));
-    if (!red.empty())
-        k_reduce<<<(int)red.size(), 256, 0, s>>>(reinterpret_cast<const RItem*>(t->d_witems.as<char>() + o1),
-                                                 (int)LEN, t->d_wpart.as<double>(), fhat); note_launch();
+        KITC_TRY(dispatch<6>(n, (int)ub_items, di, t, t->w.as<double>(), t->grid.as<double>(), fhat,
+                             t->d_wpart.as<double>(), counts, s));
+    k_reduce<<<(int)ncl, 256, 0, s>>>(dr, (int)LEN, t->d_wpart.as<double>(), fhat, counts + 1); note_launch();
+    if (upward && t->depth > 0) {
+        if (m == 3)
+            KITC_TRY(dispatch_upward<3>(n, t, tree_level_starts(t), (int)cb, fhat, s));
+        else
+            KITC_TRY(dispatch_upward<6>(n, t, tree_level_starts(t), (int)cb, fhat, s));
+    }
     KITC_CUDA(cudaGetLastError());
     return KITC_OK;
+}
+
+size_t weights_bytes(int64_t N, int64_t C, int32_t depth, int kernel, int n) {
+    int32_t m = 0;
+    if (kitc_kernel_dims(kernel, &m, nullptr) != KITC_OK || n < 1 || n > kMaxDegree) return 0;
+    const int P = n + 1;
+    const int64_t LEN = fhat_cluster_len(P, m);
+    const int sld = (3 + m + 1) & ~1;
+    const int64_t ub_items = N * (depth + 1) / kChunk + C;
+    const size_t witems = ((size_t)ub_items * sizeof(WItem) + 15) / 16 * 16 + ((size_t)C * sizeof(RItem) + 15) / 16 * 16 + 16;
+    return dev_alloc_bytes((size_t)m * N * sizeof(double)) + dev_alloc_bytes((size_t)N * sld * sizeof(double)) +
+           dev_alloc_bytes((size_t)C * 3 * P * sizeof(double)) + dev_alloc_bytes(witems) +
+           dev_alloc_bytes((size_t)std::max<int64_t>(ub_items, 1) * LEN * sizeof(double));
 }
 
 }  // namespace kitc

@@ -25,12 +25,13 @@ KITC_OK, KITC_EINVAL, KITC_ENOMEM, KITC_ECUDA, KITC_ESTATE = 0, -1, -2, -3, -4
 STOKESLET, ROTLET, STOKESLET_ROTLET = 0, 1, 2
 SELF_OMIT, SELF_INCLUDE = 0, 1
 EVAL_SIZE_CHECK = 1   # kitc_eval_flag (include/kitc.h)
+WEIGHTS_UPWARD = 1    # kitc_weights_flag
 KERNELS = {"stokeslet": STOKESLET, "rotlet": ROTLET, "stokeslet_rotlet": STOKESLET_ROTLET}
 
 # every symbol include/kitc.h declares
 EXPORTS = ("kitc_kernel_dims", "kitc_fhat_cluster_len", "kitc_tree_create", "kitc_tree_create_with_allocator",
-           "kitc_build_tree", "kitc_tree_info",
-           "kitc_tree_export", "kitc_modified_weights", "kitc_modified_weights_peers", "kitc_eval", "kitc_eval_ex", "kitc_eval_part", "kitc_eval_targets", "kitc_eval_targets_ex", "kitc_batch_targets",
+           "kitc_tree_workspace_bytes", "kitc_build_tree", "kitc_tree_info",
+           "kitc_tree_export", "kitc_modified_weights", "kitc_modified_weights_ex", "kitc_modified_weights_peers", "kitc_eval", "kitc_eval_ex", "kitc_eval_part", "kitc_eval_targets", "kitc_eval_targets_ex", "kitc_batch_targets",
            "kitc_direct", "kitc_direct_sample", "kitc_rel_error", "kitc_tree_free", "kitc_last_error",
            "kitc_launch_count")
 
@@ -76,10 +77,12 @@ def _load():
         "kitc_tree_create": [P(vp)],
         "kitc_tree_create_with_allocator": [P(KitcAllocator), P(vp)],
         "kitc_build_tree": [vp, vp, i64, i32, vp],
+        "kitc_tree_workspace_bytes": [i64, i32, i32, i32, P(C.c_size_t)],
         "kitc_tree_info": [vp, P(i64), P(i32), P(i64), P(i32)],
         "kitc_tree_export": [vp] + [vp] * 9,
         "kitc_modified_weights": [vp, i32, i32, vp, i64, i64, vp, vp],
         "kitc_modified_weights_peers": [vp, i32, i32, vp, i64, i64, vp, i32, vp],
+        "kitc_modified_weights_ex": [vp, i32, i32, vp, i64, i64, C.c_uint32, vp, vp],
         "kitc_fhat_cluster_len": [i32, i32, P(i64)],
         "kitc_eval": [vp, i32, i32, d, i32, d, i32, vp, i64, i64, vp, vp, vp],
         "kitc_eval_ex": [vp, i32, i32, d, i32, d, i32, C.c_uint32, vp, i64, i64, vp, vp, vp],
@@ -171,6 +174,12 @@ def kitc_tree_create_with_allocator(allocator=None):
     h = C.c_void_p()
     _call("kitc_tree_create_with_allocator", C.byref(allocator or TORCH_ALLOCATOR), C.byref(h))
     return h
+
+
+def kitc_tree_workspace_bytes(N, N0, kernel, n):
+    b = C.c_size_t()
+    _call("kitc_tree_workspace_bytes", int(N), int(N0), int(kernel), int(n), C.byref(b))
+    return b.value
 
 
 def kitc_build_tree(t, xyz_ptr, N, N0, stream_ptr):
@@ -269,14 +278,19 @@ class Tree:
         """[C][L]: per cluster [round][k3][comp][8 rows] (include/kitc.h)."""
         return (self.nclusters, kitc_fhat_cluster_len(kernel, n))
 
-    def modified_weights(self, kernel, n, W, cluster_range=None, fhat=None, stream=None):
+    def modified_weights(self, kernel, n, W, cluster_range=None, fhat=None, stream=None, upward=False):
+        """upward=True: KITC_WEIGHTS_UPWARD (internal clusters from their children's fhat)."""
         m, _ = kitc_kernel_dims(kernel)
         W = _dev_f64(W, m)
         if fhat is None:
             fhat = torch.empty(self.fhat_shape(kernel, n), dtype=torch.float64, device=W.device)
         _buf_f64(fhat, self.nclusters * kitc_fhat_cluster_len(kernel, n), "fhat")
         cb, ce = cluster_range if cluster_range is not None else (0, self.nclusters)
-        kitc_modified_weights(self._h, kernel, n, _ptr(W), cb, ce, _ptr(fhat), _stream(stream))
+        if upward:
+            _call("kitc_modified_weights_ex", self._h, int(kernel), int(n), _ptr(W), int(cb), int(ce),
+                  C.c_uint32(WEIGHTS_UPWARD), _ptr(fhat), _stream(stream))
+        else:
+            kitc_modified_weights(self._h, kernel, n, _ptr(W), cb, ce, _ptr(fhat), _stream(stream))
         return fhat
 
     def eval(self, kernel, n, theta, eps, fhat, out=None, batch_range=None, self_omit=True,

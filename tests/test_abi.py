@@ -155,3 +155,18 @@ int main(void) {
                            "-L", libdir, "-lkitc", f"-Wl,-rpath,{libdir}", "-o", str(exe)])
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0 and out.stdout.strip() == "ok", (out.returncode, out.stdout, out.stderr)
+
+
+def test_tree_workspace_bytes():
+    # kitc_tree_workspace_bytes: an upper bound that covers at least the sorted
+    # coordinates + scratch, the worst-case (2N - 1 clusters) table, and grows with N and n
+    from paper_1902_02250_b200 import kitc
+    b1 = kitc.kitc_tree_workspace_bytes(10_000, 100, kitc.STOKESLET, 8)
+    b2 = kitc.kitc_tree_workspace_bytes(20_000, 100, kitc.STOKESLET, 8)
+    assert b2 > b1 > 10_000 * (6 * 8 + 2 * 4)
+    assert kitc.kitc_tree_workspace_bytes(10_000, 100, kitc.STOKESLET, 10) > b1
+    assert kitc.kitc_tree_workspace_bytes(10_000, 100, kitc.STOKESLET_ROTLET, 8) > b1
+    for bad in ((0, 100, 0, 8), (10, 0, 0, 8), (10, 5, 7, 8), (10, 5, 0, 17)):
+        with pytest.raises(kitc.KitcError) as e:
+            kitc.kitc_tree_workspace_bytes(*bad)
+        assert e.value.status == kitc.KITC_EINVAL

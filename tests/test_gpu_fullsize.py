@@ -120,6 +120,12 @@ def run_config(K, name, n=None, S_tree=10_000, S_direct=10_000, direct_all_gpu=T
         dF = np.linalg.norm((Fg[1:] - F[1:]).ravel()) / np.linalg.norm(F[1:].ravel())
         rec["fhat_rel"] = float(dF)
         assert dF <= FHAT_GATE
+        # f4: the upward pass (KITC_WEIGHTS_UPWARD) against the direct Algorithm 1 fhat
+        fu = torch.zeros_like(fh)
+        G.modified_weights(kern, n, Wd, cluster_range=(1, G.nclusters), fhat=fu, upward=True)
+        Fu = fhat_to_oracle(host(fu), n)
+        rec["fhat_upward_rel"] = float(np.linalg.norm((Fu[1:] - F[1:]).ravel()) / np.linalg.norm(F[1:].ravel()))
+        assert rec["fhat_upward_rel"] <= 1e-12
         # treecode at the sampled targets
         t0 = time.time()
         ref, rst = P.treecode(kern, eps, n, theta, F, tg, stats=True)

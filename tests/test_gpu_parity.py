@@ -308,3 +308,60 @@ def test_allocator_failure_is_enomem(K):
     bad = K.KitcAllocator(K._ALLOC_FN(lambda n, s, c: None), K._RELEASE_FN(), None)   # NULL release
     hh = C.c_void_p()
     assert K.lib().kitc_tree_create_with_allocator(C.byref(bad), C.byref(hh)) == K.KITC_EINVAL
+
+
+def test_workspace_bound_covers_the_handle(K):
+    # the device memory a handle takes from its allocator stays within kitc_tree_workspace_bytes
+    for N, N0, geom in ((200_000, 500, "uniform"), (30_000, 1, "sphere")):
+        X, W = KI.particles(N, geom, seed=4)
+        Xd, Wd = dev(X), dev(W)
+        torch.cuda.synchronize()
+        before = torch.cuda.memory_allocated()
+        G = K.Tree(Xd, N0)
+        G.modified_weights(0, 8, Wd)
+        torch.cuda.synchronize()
+        held = torch.cuda.memory_allocated() - before
+        assert 0 < held <= K.kitc_tree_workspace_bytes(N, N0, 0, 8)
+        G.close()
+
+
+# ---------------------------------------------------------------- f4: upward pass for fhat
+@pytest.mark.parametrize("N,N0,n,kern,geom", [(20_000, 100, 8, 0, "uniform"), (12_000, 60, 4, 1, "sphere"),
+                                              (5436, 50, 6, 2, "rods"), (6000, 30, 3, 0, "slab"),
+                                              (3000, 40, 16, 1, "uniform"), (40, 1, 2, 0, "uniform")])
+def test_upward_weights_parity(K, N, N0, n, kern, geom):
+    # KITC_WEIGHTS_UPWARD vs the oracle's upward pass (<= 1e-13) and vs the direct Algorithm 1 (<= 1e-12)
+    m = O.DIMS[kern][0]
+    X, W = KI.particles(N, geom, seed=13, m=m)
+    T = O.Tree(X, N0)
+    U = T.modified_weights(W, n, upward=True)
+    D = T.modified_weights(W, n)
+    G = K.Tree(dev(X), N0)
+    Wd = dev(W)
+    got = fhat_to_oracle(host(G.modified_weights(kern, n, Wd, upward=True)), n)
+    for c in range(T.nclusters):
+        nu = np.linalg.norm(U[c])
+        assert np.linalg.norm(got[c] - U[c]) <= 1e-13 * max(nu, 1e-300), c
+        assert np.linalg.norm(got[c] - D[c]) <= 1e-12 * max(np.linalg.norm(D[c]), 1e-300), c
+    # suffix range (the bench's [1, C)): the same values, the root untouched
+    fh = torch.zeros(G.fhat_shape(kern, n), dtype=torch.float64, device="cuda")
+    G.modified_weights(kern, n, Wd, cluster_range=(1, G.nclusters), fhat=fh, upward=True)
+    g2 = fhat_to_oracle(host(fh), n)
+    assert np.array_equal(g2[1:], got[1:]) and not g2[0].any()
+    # the treecode with the upward fhat meets the oracle treecode (direct fhat) gate
+    out, st = G.eval(kern, n, 0.7, 0.01, G.modified_weights(kern, n, Wd, upward=True), stats=True)
+    ref, rst = T.treecode(kern, 0.01, n, 0.7, W, fhat=D, stats=True)
+    assert O.rel_error(ref, host(out)) <= 1e-10
+    assert np.array_equal(rst.astype(np.int64), host(st))
+
+
+def test_upward_range_rules(K):
+    X, W = KI.particles(5000, seed=2)
+    G = K.Tree(dev(X), 100)
+    fh = torch.zeros(G.fhat_shape(0, 4), dtype=torch.float64, device="cuda")
+    with pytest.raises(K.KitcError) as e:   # children of computed clusters must be in range
+        G.modified_weights(0, 4, dev(W), cluster_range=(0, G.nclusters - 1), fhat=fh, upward=True)
+    assert e.value.status == K.KITC_EINVAL
+    with pytest.raises(K.KitcError):        # unknown flag bits
+        K._call("kitc_modified_weights_ex", G.handle, 0, 4, K._ptr(dev(W)), 0, G.nclusters,
+                K.C.c_uint32(2), K._ptr(fh), K._stream())
