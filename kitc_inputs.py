@@ -34,6 +34,8 @@ CONFIGS = {
     "C3": dict(N=1_000_000, geometry="uniform", kernel=0, eps=0.01, n=8, theta=0.7, N0=2000),
     "C4": dict(N=1_000_000, geometry="uniform", kernel=1, eps=0.01, n=8, theta=0.7, N0=2000),
     "C5": dict(N=10_000_000, geometry="sphere", kernel=0, eps=0.005, n=8, theta=0.7, N0=2000),
+    # BASELINE config 4 at its other degree (n in {4, 8})
+    "C4n4": dict(N=1_000_000, geometry="uniform", kernel=1, eps=0.01, n=4, theta=0.7, N0=2000),
     # not a BASELINE config: the paper's own Example 2 parallel run (Table 5):
     # 80^2 rods x 151 points, Stokeslet + rotlet, eps = 0.3, theta = 0.7, n = 7, N0 = 1000
     "X2": dict(N=966_400, geometry="rods", kernel=2, eps=0.3, n=7, theta=0.7, N0=1000),

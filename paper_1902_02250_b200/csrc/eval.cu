@@ -759,7 +759,10 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
                     }
                 }
             } else {
-                // children pushed in reverse so the first child is popped first (A17)
+                // children pushed in reverse so the first child is popped first (A17).  The
+                // stack holds <= 7 depth + 1 entries (8 (depth + 1) allocated); overflowing it
+                // would be a library bug: trap (the next synchronising call reports KITC_ECUDA)
+                if (sp + tp.w > a.stack_cap) __trap();
                 if (lane < tp.w) stk[sp + tp.w - 1 - lane] = make_int2(tp.z + lane, (int)rm);
                 sp += tp.w;
                 __syncwarp();
