@@ -569,6 +569,84 @@ __device__ __forceinline__ void near_field_impl(double x, double y, double z, in
     }
 }
 
+#ifndef KITC_NEAR_TB
+// kernels (bit k = kernel k) whose near field is blocked over target pairs: the rotlet (C4n4, n = 4:
+// 57.9 -> 55.4 ms; C4, n = 8: 140.7 -> 140.3 ms); slower for the Stokeslet (C3 +0.5%) and the
+// combined kernel (X2 +0.5%)
+#define KITC_NEAR_TB 2
+#endif
+#ifndef KITC_NEAR_TB_U
+#define KITC_NEAR_TB_U 2
+#endif
+// Near field blocked over target pairs: the lane of rank rk (of TS) sums sources
+// b + rk, b + rk + TS, ... for TWO targets A and B, so every source record it loads
+// feeds two pair evaluations (half the loads per pair, two independent chains).
+// SELF: A or B may be a source of this leaf (pair with f = 0, s = 1: exact zero).
+template <int KER, bool SELF>
+__device__ __forceinline__ void near_field_tb(double xa, double ya, double za, int ta, double xb, double yb,
+                                              double zb, int tb, int b, int e, int rk, int TS, const EvalArgs& a,
+                                              double* accA, double* accB) {
+    using K = EvalKern<KER>;
+    constexpr int M = K::M, U = KITC_NEAR_TB_U, NQ = (3 + M + 1) / 2;
+    int j = b + rk;
+    for (; j + (U - 1) * TS < e; j += U * TS) {
+        double v[U][NQ * 2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const double2* r = reinterpret_cast<const double2*>(a.src + (size_t)(j + u * TS) * a.sld);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const double2 d2 = __ldg(r + q);
+                v[u][2 * q] = d2.x;
+                v[u][2 * q + 1] = d2.y;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int jj = j + u * TS;
+            {
+                const bool me = SELF && jj == ta;
+                double f[M];
+#pragma unroll
+                for (int m = 0; m < M; ++m) f[m] = SELF && me ? 0.0 : v[u][3 + m];
+                const double dx = xa - v[u][0], dy = ya - v[u][1], dz = za - v[u][2];
+                const double s = me ? 1.0 : fma(dx, dx, fma(dy, dy, fma(dz, dz, a.kp.e2)));
+                K::pair(dx, dy, dz, s, f, accA, a.kp);
+            }
+            {
+                const bool me = SELF && jj == tb;
+                double f[M];
+#pragma unroll
+                for (int m = 0; m < M; ++m) f[m] = SELF && me ? 0.0 : v[u][3 + m];
+                const double dx = xb - v[u][0], dy = yb - v[u][1], dz = zb - v[u][2];
+                const double s = me ? 1.0 : fma(dx, dx, fma(dy, dy, fma(dz, dz, a.kp.e2)));
+                K::pair(dx, dy, dz, s, f, accB, a.kp);
+            }
+        }
+    }
+    for (; j < e; j += TS) {
+        const double2* r = reinterpret_cast<const double2*>(a.src + (size_t)j * a.sld);
+        double v[NQ * 2];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const double2 d2 = __ldg(r + q);
+            v[2 * q] = d2.x;
+            v[2 * q + 1] = d2.y;
+        }
+        const bool mea = SELF && j == ta, meb = SELF && j == tb;
+        double fa[M], fb[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            fa[m] = mea ? 0.0 : v[3 + m];
+            fb[m] = meb ? 0.0 : v[3 + m];
+        }
+        const double dxa = xa - v[0], dya = ya - v[1], dza = za - v[2];
+        const double dxb = xb - v[0], dyb = yb - v[1], dzb = zb - v[2];
+        K::pair(dxa, dya, dza, mea ? 1.0 : fma(dxa, dxa, fma(dya, dya, fma(dza, dza, a.kp.e2))), fa, accA, a.kp);
+        K::pair(dxb, dyb, dzb, meb ? 1.0 : fma(dxb, dxb, fma(dyb, dyb, fma(dzb, dzb, a.kp.e2))), fb, accB, a.kp);
+    }
+}
+
 // The self pair can only occur in the leaf holding the target; every other leaf
 // runs the select-free loop (warp-uniform: a batch never straddles leaves).
 template <int KER>
@@ -595,6 +673,32 @@ __device__ __forceinline__ void near_leaf(double x, double y, double z, int t, i
     const int grp = lane % kGroup, g = lane / kGroup;
     const int nt = __popc(rm) / kGroup;
     const bool mine = (rm >> lane) & 1u;
+    if (((KITC_NEAR_TB >> KER) & 1) && nt >= 3) {
+        // 3 or 4 participating targets: each half-warp takes the target pair of its two groups,
+        // 16 lanes striding the sources, every record feeding both targets; a lane's partial for
+        // the partner group's target is handed over with one shuffle (lane ^ 8).  A target that
+        // does not take this leaf directly (nt = 3) is computed and discarded.
+        const int la = (lane >> 4) * 16, lb = la + kGroup;
+        const double xa = __shfl_sync(0xffffffffu, x, la), ya = __shfl_sync(0xffffffffu, y, la);
+        const double za = __shfl_sync(0xffffffffu, z, la);
+        const double xb = __shfl_sync(0xffffffffu, x, lb), yb = __shfl_sync(0xffffffffu, y, lb);
+        const double zb = __shfl_sync(0xffffffffu, z, lb);
+        const int ta = __shfl_sync(0xffffffffu, t, la), tb = __shfl_sync(0xffffffffu, t, lb);
+        double accA[NA], accB[NA];
+#pragma unroll
+        for (int c = 0; c < NA; ++c) accA[c] = accB[c] = 0.0;
+        if (a.self_omit && t >= b && t < e)  // warp-uniform: the batch's leaf
+            near_field_tb<KER, true>(xa, ya, za, ta, xb, yb, zb, tb, b, e, lane & 15, 16, a, accA, accB);
+        else
+            near_field_tb<KER, false>(xa, ya, za, -1, xb, yb, zb, -1, b, e, lane & 15, 16, a, accA, accB);
+        const bool inB = (lane & kGroup) != 0;
+#pragma unroll
+        for (int c = 0; c < NA; ++c) {
+            const double other = __shfl_xor_sync(0xffffffffu, inB ? accA[c] : accB[c], kGroup);
+            if (mine) acc[c] += (inB ? accB[c] : accA[c]) + other;
+        }
+        return;
+    }
     if (!KITC_NEAR_TEAMS || nt >= 3) {
         if (mine) near_field<KER>(x, y, z, t, b, e, grp, kGroup, a, acc);
         return;
