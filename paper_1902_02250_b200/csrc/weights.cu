@@ -28,7 +28,16 @@ namespace {
 #ifndef KITC_W_MINB
 #define KITC_W_MINB 6  // resident CTAs per SM (n <= 10); measured: 6 > 1 (128 regs) > 8 > 10
 #endif
-constexpr int kChunk = 4096;  // particles per work item
+constexpr int kChunk = 4096;       // particles per work item (large calls)
+constexpr int kChunkSmall = 1024;  // ... when the call has too few items to fill the GPU
+// Chunk size of a tree: small chunks when the whole tree holds fewer than ~2 waves of work items
+// (N ~ 1e6: a rank's shard at 8 GPUs then still fills the GPU; measured C3 8-rank shard 0.62 ->
+// 0.36 ms), large ones otherwise (fewer partial slots to sum; C5 17.2 ms vs 18.2 ms with small
+// chunks).  It depends on the tree only, never on the cluster range, so fhat (and every result) is
+// bitwise the same however the clusters are split over calls or ranks.
+static int weights_chunk(int64_t particle_clusters) {
+    return particle_clusters / kChunk < 2 * 148 * KITC_W_MINB ? kChunkSmall : kChunk;
+}
 #ifndef KITC_W_TILE
 #define KITC_W_TILE 32  // measured: 32 > 64 > 16
 #endif
@@ -205,10 +214,10 @@ __global__ void k_reduce(const RItem* __restrict__ r, int len, const double* __r
 }
 
 // Work items of clusters [cb, ce) built on the device (one CTA): per cluster
-// nch = ceil(N_C / kChunk) chunks; one chunk writes fhat directly, several write
+// nch = ceil(N_C / chunk) chunks; one chunk writes fhat directly, several write
 // partial slots that k_reduce sums in chunk order.  counts[0] = items, [1] = reduce
 // entries.  Exclusive scans in cluster order (three at once).
-__global__ void __launch_bounds__(1024) k_witems(const int4* __restrict__ topo, int cb, int ce, int leaves_only,
+__global__ void __launch_bounds__(1024) k_witems(const int4* __restrict__ topo, int cb, int ce, int leaves_only, int chunk,
                                                  WItem* __restrict__ items, RItem* __restrict__ red,
                                                  int* __restrict__ counts) {
     __shared__ int3 wsum[33];
@@ -220,7 +229,7 @@ __global__ void __launch_bounds__(1024) k_witems(const int4* __restrict__ topo, 
         int nch = 0;
         if (c < ce) {
             tp = topo[c];
-            nch = (leaves_only && tp.w > 0) ? 0 : (tp.y - tp.x + kChunk - 1) / kChunk;
+            nch = (leaves_only && tp.w > 0) ? 0 : (tp.y - tp.x + chunk - 1) / chunk;
         }
         const int3 v = make_int3(nch, nch > 1 ? nch : 0, nch > 1 ? 1 : 0);
         int3 inc = v;
@@ -251,7 +260,7 @@ __global__ void __launch_bounds__(1024) k_witems(const int4* __restrict__ topo, 
             const int io = run.x + wsum[w].x + inc.x - v.x, so = run.y + wsum[w].y + inc.y - v.y,
                       ro = run.z + wsum[w].z + inc.z - v.z;
             for (int q = 0; q < nch; ++q)
-                items[io + q] = WItem{c, tp.x + q * kChunk, min(tp.y, tp.x + (q + 1) * kChunk), nch == 1 ? -1 : so + q};
+                items[io + q] = WItem{c, tp.x + q * chunk, min(tp.y, tp.x + (q + 1) * chunk), nch == 1 ? -1 : so + q};
             if (nch > 1) red[ro] = RItem{c, so, nch, 0};
         }
         run.x += wsum[32].x;
@@ -442,14 +451,16 @@ kitc_status modified_weights(kitc_tree* t, int kernel, int n, const double* w, i
     // work items on the device; grids sized by upper bounds (items: each particle lies in
     // depth + 1 clusters, each cluster adds at most one partial chunk) -- no host sync
     const int64_t ncl = ce - cb;
-    const int64_t ub_items = std::min<int64_t>((int64_t)N * (t->depth + 1) / kChunk + ncl, 0x7fffffff);
+    const int chunk = weights_chunk((int64_t)N * (t->depth + 1));
+    const int64_t ub_items = std::min<int64_t>((int64_t)N * (t->depth + 1) / chunk + ncl, 0x7fffffff);
     const size_t o1 = ((size_t)ub_items * sizeof(WItem) + 15) / 16 * 16;
     const size_t o2 = o1 + ((size_t)ncl * sizeof(RItem) + 15) / 16 * 16;
     KITC_TRY(t->d_witems.ensure(o2 + 16, s));
     WItem* di = t->d_witems.as<WItem>();
     RItem* dr = reinterpret_cast<RItem*>(t->d_witems.as<char>() + o1);
     int* counts = reinterpret_cast<int*>(t->d_witems.as<char>() + o2);
-    k_witems<<<1, 1024, 0, s>>>(t->topo.as<int4>(), (int)cb, (int)ce, upward ? 1 : 0, di, dr, counts); note_launch();
+    k_witems<<<1, 1024, 0, s>>>(t->topo.as<int4>(), (int)cb, (int)ce, upward ? 1 : 0, chunk, di, dr, counts);
+    note_launch();
     KITC_TRY(t->d_wpart.ensure((size_t)std::max<int64_t>(ub_items, 1) * LEN * sizeof(double), s));
     if (m == 3)
         KITC_TRY(dispatch<3>(n, (int)ub_items, di, t, t->w.as<double>(), t->grid.as<double>(), fhat,
@@ -474,7 +485,7 @@ size_t weights_bytes(int64_t N, int64_t C, int32_t depth, int kernel, int n) {
     const int P = n + 1;
     const int64_t LEN = fhat_cluster_len(P, m);
     const int sld = (3 + m + 1) & ~1;
-    const int64_t ub_items = N * (depth + 1) / kChunk + C;
+    const int64_t ub_items = N * (depth + 1) / kChunkSmall + C;
     const size_t witems = ((size_t)ub_items * sizeof(WItem) + 15) / 16 * 16 + ((size_t)C * sizeof(RItem) + 15) / 16 * 16 + 16;
     return dev_alloc_bytes((size_t)m * N * sizeof(double)) + dev_alloc_bytes((size_t)N * sld * sizeof(double)) +
            dev_alloc_bytes((size_t)C * 3 * P * sizeof(double)) + dev_alloc_bytes(witems) +
