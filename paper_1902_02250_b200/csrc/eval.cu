@@ -75,7 +75,10 @@ __host__ __device__ constexpr int eval_min_blocks() {  // CTAs/SM per instantiat
     return KER == 0 ? (PT == 9 ? KITC_EVAL_MINB : (PT == 8 || PT >= 10) ? KITC_EVAL_MINB_P8 : KITC_EVAL_MINB_OTHER)
                     : KITC_EVAL_MINB1;
 }
-constexpr int kPartChunk = 64;          // batches per chunk of the interleaved multi-GPU split
+#ifndef KITC_PART_CHUNK
+#define KITC_PART_CHUNK 64
+#endif
+constexpr int kPartChunk = KITC_PART_CHUNK;  // batches per chunk of the interleaved multi-GPU split
 #ifdef KITC_EVAL_HIST
 __device__ unsigned long long g_hist[10];
 }  // namespace
