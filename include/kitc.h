@@ -208,7 +208,10 @@ kitc_status kitc_modified_weights_peers(kitc_tree* t, int32_t kernel, int32_t n,
  *  fhat_dev: the FULL double[C][L] of kitc_modified_weights (every cluster),
  *  16-byte aligned (else EINVAL).
  *  out_dev: device double[N][p], original order; only the targets of the given
- *  batches are written.
+ *  batches are written.  It may also be pinned host memory (cudaMallocHost /
+ *  cudaHostAlloc, mapped into the device address space under unified
+ *  addressing): each target's row is then written over the host link as the
+ *  kernel finishes it (zero-copy; the caller synchronises before reading).
  *  stats_dev: optional (NULL = off) device uint64[N][5], original order:
  *  far clusters, far pairs, near leaves, near pairs, covered sources. */
 kitc_status kitc_eval(const kitc_tree* t, int32_t kernel, int32_t n, double theta, int32_t N0,

@@ -140,10 +140,12 @@ def _dev_f64(t, shape1):
     return t
 
 
-def _buf_f64(t, numel, what):
-    """A caller-provided device buffer the kernels index: contiguous fp64 CUDA, exact size."""
-    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
-        raise ValueError(f"{what}: expected a contiguous float64 CUDA tensor")
+def _buf_f64(t, numel, what, host_ok=False):
+    """A caller-provided buffer the kernels index: contiguous fp64 CUDA (or, host_ok, pinned host
+    memory -- mapped into the device address space under unified addressing), exact size."""
+    where = t.is_cuda or (host_ok and t.is_pinned())
+    if not (where and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError(f"{what}: expected a contiguous float64 CUDA tensor" + (" or pinned host tensor" if host_ok else ""))
     if t.numel() != numel:
         raise ValueError(f"{what}: expected {numel} elements, got {t.numel()}")
     return t
@@ -295,13 +297,14 @@ class Tree:
 
     def eval(self, kernel, n, theta, eps, fhat, out=None, batch_range=None, self_omit=True,
              stats=False, stream=None, size_check=False, part=None):
-        """part=(p, k): interleaved part p of k (kitc_eval_part) instead of a batch range."""
+        """part=(p, k): interleaved part p of k (kitc_eval_part) instead of a batch range.
+        out may be a pinned host tensor: the kernel then writes the rows straight to host memory."""
         _, p = kitc_kernel_dims(kernel)
         _buf_f64(fhat, self.nclusters * kitc_fhat_cluster_len(kernel, n), "fhat")
         dev = fhat.device
         if out is None:
             out = torch.zeros((self.N, p), dtype=torch.float64, device=dev)
-        _buf_f64(out, self.N * p, "out")
+        _buf_f64(out, self.N * p, "out", host_ok=True)
         st = torch.zeros((self.N, 5), dtype=torch.int64, device=dev) if stats else None
         if part is not None:
             _call("kitc_eval_part", self._h, int(kernel), int(n), float(theta), self.N0, float(eps),

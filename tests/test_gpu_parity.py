@@ -365,3 +365,17 @@ def test_upward_range_rules(K):
     with pytest.raises(K.KitcError):        # unknown flag bits
         K._call("kitc_modified_weights_ex", G.handle, 0, 4, K._ptr(dev(W)), 0, G.nclusters,
                 K.C.c_uint32(2), K._ptr(fh), K._stream())
+
+
+def test_eval_into_pinned_host_output(K):
+    # kitc_eval may write its rows straight into pinned host memory (zero-copy): identical values
+    X, W = KI.particles(30_000, seed=6)
+    G = K.Tree(dev(X), 300)
+    fh = G.modified_weights(0, 6, dev(W))
+    ref = host(G.eval(0, 6, 0.7, 0.01, fh))
+    outh = torch.zeros((30_000, 3), dtype=torch.float64).pin_memory()
+    G.eval(0, 6, 0.7, 0.01, fh, out=outh)
+    torch.cuda.synchronize()
+    assert np.array_equal(outh.numpy(), ref)
+    with pytest.raises(ValueError):          # pageable host memory is refused by the binding
+        G.eval(0, 6, 0.7, 0.01, fh, out=torch.zeros((30_000, 3), dtype=torch.float64))
