@@ -34,7 +34,8 @@ namespace {
 #define KITC_EVAL_WARPS 4
 #endif
 #ifndef KITC_EVAL_MINB
-#define KITC_EVAL_MINB 5  // resident CTAs per SM (register budget), Stokeslet (measured: 5 > 4 > 6 with dz in smem)
+#define KITC_EVAL_MINB 4  // resident CTAs per SM (register budget), Stokeslet at n = 8 (round 2: 4 CTAs with the
+                          // target-pair near field (below) beat 5 CTAs without it: C3 95.0 -> 93.8 ms)
 #endif
 #ifndef KITC_EVAL_MINB_P8
 #define KITC_EVAL_MINB_P8 4  // Stokeslet at n = 7, 9, 10 (measured: 4 beats 5 on X1 / X1L and the C2 sweep)
@@ -68,6 +69,9 @@ namespace {
 // P = 8, 10 (measured on the C3 input: n = 7 -8%, n = 9 -6%; slower at P = 9 (spills at
 // 5 CTAs/SM, 4 CTAs/SM loses more), P = 11, P <= 7 and for the rotlet)
 #define KITC_FAR_TB 1
+#endif
+#ifndef KITC_FAR_TB_P9
+#define KITC_FAR_TB_P9 0  // tuning builds only (with KITC_EVAL_MINB=4: no spills)
 #endif
 constexpr int kWarps = KITC_EVAL_WARPS;  // warps (batches) per CTA
 template <int PT, int KER>
@@ -211,7 +215,7 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
     // stage for its own target (acc) and for the sibling target of lane L ^ 8 (oth); the
     // f-hat row is read once for both, and oth is folded into the sibling's lanes below
     constexpr bool kTB = KITC_FAR_TB && KITC_DZ_SMEM && K::kPairRows && kSB == 2 && KER == 0 &&
-                         (PT == 8 || PT == 10);
+                         (PT == 8 || PT == 10 || (KITC_FAR_TB_P9 && PT == 9));
     const bool tb = kTB && am == 0xffffffffu;
     double oth[K::NA];
     double ox = 0.0, oy = 0.0;
@@ -578,8 +582,16 @@ __device__ __forceinline__ void near_field_impl(double x, double y, double z, in
 // combined kernel (X2 +0.5%)
 #define KITC_NEAR_TB 2
 #endif
-#ifndef KITC_NEAR_TB_U
-#define KITC_NEAR_TB_U 2
+#ifndef KITC_NEAR_TB_AT4
+// also the Stokeslet instantiations that run at 4 CTAs/SM (128 registers: the record loads of 4 sources
+// stay in flight for 2 targets): C3 95.0 -> 93.8 ms, X1 40.2 -> 39.5 ms, C5 856.8 -> 858.8 ms
+#define KITC_NEAR_TB_AT4 1
+#endif
+#ifndef KITC_NEAR_TB_U0
+#define KITC_NEAR_TB_U0 4  // Stokeslet: source records per lane in flight (C3, 4 CTAs/SM: U = 3, 4, 6, 8 -> 93.9, 93.7, 94.5, 96.8 ms)
+#endif
+#ifndef KITC_NEAR_TB_U1
+#define KITC_NEAR_TB_U1 2  // rotlet
 #endif
 // Near field blocked over target pairs: the lane of rank rk (of TS) sums sources
 // b + rk, b + rk + TS, ... for TWO targets A and B, so every source record it loads
@@ -590,7 +602,7 @@ __device__ __forceinline__ void near_field_tb(double xa, double ya, double za, i
                                               double zb, int tb, int b, int e, int rk, int TS, const EvalArgs& a,
                                               double* accA, double* accB) {
     using K = EvalKern<KER>;
-    constexpr int M = K::M, U = KITC_NEAR_TB_U, NQ = (3 + M + 1) / 2;
+    constexpr int M = K::M, U = KER == 0 ? KITC_NEAR_TB_U0 : KITC_NEAR_TB_U1, NQ = (3 + M + 1) / 2;
     int j = b + rk;
     for (; j + (U - 1) * TS < e; j += U * TS) {
         double v[U][NQ * 2];
@@ -668,7 +680,7 @@ __device__ __forceinline__ void near_field(double x, double y, double z, int t, 
 // and the team's partial sums are folded into the owning group's lanes with
 // butterfly shuffles -- the per-target result is the same sum (rounding order
 // aside), with no idle lanes.  Called by ALL lanes of the warp.
-template <int KER>
+template <int KER, int PT>
 __device__ __forceinline__ void near_leaf(double x, double y, double z, int t, int b, int e, int lane, unsigned rm,
                                           const EvalArgs& a, double* acc) {
     using K = EvalKern<KER>;
@@ -676,7 +688,9 @@ __device__ __forceinline__ void near_leaf(double x, double y, double z, int t, i
     const int grp = lane % kGroup, g = lane / kGroup;
     const int nt = __popc(rm) / kGroup;
     const bool mine = (rm >> lane) & 1u;
-    if (((KITC_NEAR_TB >> KER) & 1) && nt >= 3) {
+    constexpr bool kTB = ((KITC_NEAR_TB >> KER) & 1) ||
+                         (KITC_NEAR_TB_AT4 && KER == 0 && eval_min_blocks<PT, KER>() == 4);
+    if (kTB && nt >= 3) {
         // 3 or 4 participating targets: each half-warp takes the target pair of its two groups,
         // 16 lanes striding the sources, every record feeding both targets; a lane's partial for
         // the partner group's target is handed over with one shuffle (lane ^ 8).  A target that
@@ -856,7 +870,7 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
         }
         if (rm) {
             if (tp.w == 0) {
-                near_leaf<KER>(x, y, z, t, tp.x, tp.y, lane, rm, a, acc);
+                near_leaf<KER, PT>(x, y, z, t, tp.x, tp.y, lane, rm, a, acc);
                 if (in && !ok) {
                     if (STATS) {
                         const int self = (a.self_omit && t >= tp.x && t < tp.y) ? 1 : 0;
