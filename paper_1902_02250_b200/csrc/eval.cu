@@ -64,6 +64,9 @@ namespace {
 #ifndef KITC_EVAL_SB
 #define KITC_EVAL_SB 2
 #endif
+#ifndef KITC_ROWPF
+#define KITC_ROWPF 1  // far field: load the next stage's row grid coordinates one stage ahead (see kRowPF)
+#endif
 #ifndef KITC_FAR_TB
 // far field with all 4 targets accepting: one row for TWO targets per lane, Stokeslet at
 // P = 8, 10 (measured on the C3 input: n = 7 -8%, n = 9 -6%; slower at P = 9 (spills at
@@ -226,6 +229,21 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
         oy = __shfl_xor_sync(0xffffffffu, y, kGroup);
     }
 #endif
+    // the Stokeslet's 4-CTA/SM instantiations without target-pair blocking (128 registers) keep the
+    // grid coordinates (x of k1, y of k2) of the lane's two rows of the NEXT two-block stage in
+    // registers: C3 93.8 -> 93.4 ms, C5 857.7 -> 854.3 ms (slower for the rotlet and at P = 8)
+    constexpr bool kRowPF = KITC_ROWPF && KER == 0 && eval_min_blocks<PT, KER>() == 4 && PT != 8 && PT != 10;
+    double rg[4];
+    auto row_grid = [&](int sq) {
+        const int ra = (sq * kSB + (grp >> 2)) * kRows + 2 * (grp & 3);
+        const int k1a = ra / P, k2a = ra - k1a * P;
+        const int k1b = k2a + 1 == P ? k1a + 1 : k1a, k2b = k2a + 1 == P ? 0 : k2a + 1;
+        rg[0] = __ldg(g + k1a);
+        rg[1] = __ldg(g + P + k2a);
+        rg[2] = __ldg(g + k1b);
+        rg[3] = __ldg(g + P + k2b);
+    };
+    if constexpr (kRowPF) row_grid(0);
     for (int st = 0; st < NS; ++st) {
         const int k = base + st;
         const double* B = ws.buf + (k & 1) * kSB * blk;
@@ -261,11 +279,22 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
         if (K::kPairRows && kSB == 2 && b0 + 1 < RF) {
             // two full blocks: rows ra, ra + 1 of block h = grp / 4
             const int h = grp >> 2, j = 2 * (grp & 3);
-            const int ra = (b0 + h) * kRows + j;
-            const int k1a = ra / P, k2a = ra - k1a * P;
-            const int k1b = k2a + 1 == P ? k1a + 1 : k1a, k2b = k2a + 1 == P ? 0 : k2a + 1;
-            const double dxa = x - __ldg(g + k1a), dya = y - __ldg(g + P + k2a);
-            const double dxb = x - __ldg(g + k1b), dyb = y - __ldg(g + P + k2b);
+            double dxa, dya, dxb, dyb;
+            if constexpr (kRowPF) {  // loaded during the previous stage
+                dxa = x - rg[0];
+                dya = y - rg[1];
+                dxb = x - rg[2];
+                dyb = y - rg[3];
+                if (st + 1 < NS) row_grid(st + 1);
+            } else {
+                const int ra = (b0 + h) * kRows + j;
+                const int k1a = ra / P, k2a = ra - k1a * P;
+                const int k1b = k2a + 1 == P ? k1a + 1 : k1a, k2b = k2a + 1 == P ? 0 : k2a + 1;
+                dxa = x - __ldg(g + k1a);
+                dya = y - __ldg(g + P + k2a);
+                dxb = x - __ldg(g + k1b);
+                dyb = y - __ldg(g + P + k2b);
+            }
             const double pa = fma(dya, dya, dxa * dxa) + kp.e2;
             const double pb = fma(dyb, dyb, dxb * dxb) + kp.e2;
             const double* Bh = B + h * blk + j;
