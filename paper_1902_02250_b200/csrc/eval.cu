@@ -61,6 +61,9 @@ namespace {
 #ifndef KITC_DZ_SMEM
 #define KITC_DZ_SMEM 1  // far field: per-plane dz of the batch's targets in shared memory
 #endif
+#ifndef KITC_DZ_REG9
+#define KITC_DZ_REG9 1  // ... but in registers for these kernels (bit k) at P = 9 (4 CTAs/SM, 128 registers)
+#endif
 #ifndef KITC_EVAL_SB
 #define KITC_EVAL_SB 2
 #endif
@@ -201,18 +204,19 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
         issue(0, base);
         if (NS > 1) issue(1, base + 1);
     }
-#if KITC_DZ_SMEM
-    // dz per plane of this lane's target, in shared memory (frees registers)
-    double* dz = ws.dzs + (lane / kGroup) * P;
-    for (int k3 = grp; k3 < P; k3 += kGroup) dz[k3] = z - __ldg(g + 2 * P + k3);
-    __syncwarp(am);
-#else
-    double dz[PT > 0 ? PT : 1];
-    if constexpr (PT > 0) {
+    // dz per plane of this lane's target: in shared memory (frees registers; the target-pair
+    // path also reads the sibling's), or in registers where the budget allows (kDzReg)
+    constexpr bool kDzReg = PT > 0 && (!KITC_DZ_SMEM || (((KITC_DZ_REG9 >> KER) & 1) && PT == 9));
+    double dzr[PT > 0 ? PT : 1];
+    double* dzp = ws.dzs + (lane / kGroup) * P;
+    if constexpr (kDzReg) {
 #pragma unroll
-        for (int k3 = 0; k3 < PT; ++k3) dz[k3] = z - __ldg(g + 2 * PT + k3);
+        for (int k3 = 0; k3 < (PT > 0 ? PT : 1); ++k3) dzr[k3] = z - __ldg(g + 2 * P + k3);
+    } else {
+        for (int k3 = grp; k3 < P; k3 += kGroup) dzp[k3] = z - __ldg(g + 2 * P + k3);
+        __syncwarp(am);
     }
-#endif
+#define KITC_DZ(k3) (kDzReg ? dzr[k3] : dzp[k3])
 #if KITC_FAR_TB
     // register blocking over targets (all 4 accept): lane L evaluates row L & 15 of the
     // stage for its own target (acc) and for the sibling target of lane L ^ 8 (oth); the
@@ -267,7 +271,7 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
                     double f[M];
 #pragma unroll
                     for (int m = 0; m < M; ++m) f[m] = Bj[(k3 * M + m) * kRows];
-                    const double za = dz[k3], zb = dzb[k3];
+                    const double za = KITC_DZ(k3), zb = dzb[k3];
                     K::pair_row(dxa, dya, za, fma(za, za, pa), f, acc, rA, kp);
                     K::pair_row(dxb, dyb, zb, fma(zb, zb, pb), f, oth, rB, kp);
                 }
@@ -309,8 +313,9 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
                         fa[m] = v.x;
                         fb[m] = v.y;
                     }
-                    K::pair_row(dxa, dya, dz[k3], fma(dz[k3], dz[k3], pa), fa, acc, rA, kp);
-                    K::pair_row(dxb, dyb, dz[k3], fma(dz[k3], dz[k3], pb), fb, acc, rB, kp);
+                    const double zk = KITC_DZ(k3);
+                    K::pair_row(dxa, dya, zk, fma(zk, zk, pa), fa, acc, rA, kp);
+                    K::pair_row(dxb, dyb, zk, fma(zk, zk, pb), fb, acc, rB, kp);
                 }
             } else {
                 for (int k3 = 0; k3 < P; ++k3) {
@@ -343,7 +348,8 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
                             double f[M];
 #pragma unroll
                             for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + grp];
-                            K::pair_row(dx, dy, dz[k3], fma(dz[k3], dz[k3], pxye), f, acc, r, kp);
+                            const double zk = KITC_DZ(k3);
+                            K::pair_row(dx, dy, zk, fma(zk, zk, pxye), f, acc, r, kp);
                         }
                     } else {
                         for (int k3 = 0; k3 < P; ++k3) {
@@ -355,7 +361,7 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
                         }
                     }
                     K::row_end(dx, dy, r, acc);
-                } else if (KITC_DZ_SMEM && (P2 - RF * kRows == 2 || P2 - RF * kRows == 4)) {
+                } else if (!kDzReg && (P2 - RF * kRows == 2 || P2 - RF * kRows == 4)) {
                     // partial block of 2 or 4 rows (even P): kRows / nrem lanes per row, each
                     // summing a contiguous k3 range in row form (partial row sums are linear)
                     const int nrem = P2 - RF * kRows, L = kRows / max(nrem, 1), KL = (P + L - 1) / L;
@@ -368,7 +374,7 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
                         double f[M];
 #pragma unroll
                         for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + jj];
-                        K::pair_row(dx, dy, dz[k3], fma(dz[k3], dz[k3], pxye), f, acc, r, kp);
+                        K::pair_row(dx, dy, dzp[k3], fma(dzp[k3], dzp[k3], pxye), f, acc, r, kp);
                     }
                     K::row_end(dx, dy, r, acc);
                 } else {  // partial last block: pair by pair
@@ -400,6 +406,7 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
     }
 #endif
     __syncwarp(am);
+#undef KITC_DZ
 }
 
 // Far field of one cluster accepted by only 1 or 2 of the batch's targets, by the
