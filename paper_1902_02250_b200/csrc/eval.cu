@@ -41,7 +41,7 @@ namespace {
 #define KITC_EVAL_MINB_P8 4  // Stokeslet at n = 7, 9, 10 (measured: 4 beats 5 on X1 / X1L and the C2 sweep)
 #endif
 #ifndef KITC_EVAL_MINB_OTHER
-#define KITC_EVAL_MINB_OTHER 5  // Stokeslet at n <= 6 (measured: 5 beats 4 on the C2 sweep)
+#define KITC_EVAL_MINB_OTHER 4  // Stokeslet at n <= 6 (round 2, with the target-pair near field: n = 3, 5, 6 on the C3 input 32.6 -> 30.6, 49.7 -> 47.6, 59.6 -> 59.1 ms; n = 4 39.6 both)
 #endif
 #ifndef KITC_EVAL_MINB1
 #define KITC_EVAL_MINB1 4  // rotlet / combined (measured: 4 beats 5 and 6 on C4)
