@@ -82,13 +82,27 @@ class ClockSampler:
         self.path = os.path.join("/tmp", f"kitc_clocks_{os.getpid()}.csv")
 
     def start(self):
+        """Start nvidia-smi and wait (<= 5 s) until it has produced its first line, so that the
+        samples taken from `mark()` on cover the timed region even when it is short."""
         try:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and os.path.getsize(self.path) == 0:
+                time.sleep(0.01)
         except Exception:
             self.p = None
+        self.pos = 0
+
+    def mark(self):
+        """The timed region starts: later lines only."""
+        try:
+            self.f.flush()
+            self.pos = os.path.getsize(self.path)
+        except Exception:
+            self.pos = 0
 
     def stop(self):
         if self.p is None:
@@ -98,7 +112,10 @@ class ClockSampler:
         self.f.close()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        with open(self.path) as fh:
+            fh.seek(self.pos)
+            lines = fh.read().splitlines()
+        for line in lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -374,6 +391,7 @@ def run_kitc(args, cfg, rank, world, local_rank):
     barrier()
     clk = ClockSampler(local_rank)
     clk.start()
+    clk.mark()
     l0 = kitc.kitc_launch_count()
     tot_ms, eval_ms = 0.0, 0.0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

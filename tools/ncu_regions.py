@@ -10,9 +10,19 @@ import sys
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-EVAL = [(133, 157, "TMA / mbarrier helpers"), (171, 364, "far field: staging, row setup, stage loop"),
-        (365, 512, "far field teams (1-2 accepting targets)"), (513, 573, "near field loop (loads)"),
-        (574, 640, "near field dispatch / teams"), (641, 820, "traversal (MAC, stack, epilogue)")]
+ROOT = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+NAMES = {"tma_round": "TMA / mbarrier helpers", "mbar_wait": "TMA / mbarrier helpers",
+         "smem_u32": "TMA / mbarrier helpers", "far_field": "far field: staging, row setup, stage loop",
+         "far_field_team": "far field teams (1-2 accepting targets)",
+         "near_field_tb": "near field loop, target pairs (loads)", "near_field_impl": "near field loop (loads)",
+         "near_field": "near field dispatch / teams", "near_leaf": "near field dispatch / teams",
+         "k_eval": "traversal (MAC, stack, epilogue)", "__launch_bounds__": "traversal (MAC, stack, epilogue)"}
+# function of every line of eval.cu (the source the capture was built from): the last definition above it
+EVAL = []
+for i, ln in enumerate(open(__import__("os").path.join(ROOT, "paper_1902_02250_b200", "csrc", "eval.cu")), 1):
+    m = re.search(r"__(?:device|global)__.*?\b(\w+)\(", ln)
+    if m and not ln.lstrip().startswith("//"):
+        EVAL.append((i, m.group(1)))
 
 
 def region(f, ln):
@@ -25,9 +35,11 @@ def region(f, ln):
             return "pair math, far field rows"
         return "pair.cuh other"
     if f == "eval.cu":
-        for a, b, n in EVAL:
-            if a <= ln <= b:
-                return n
+        name = None
+        for start, fn in EVAL:
+            if start <= ln:
+                name = fn
+        return NAMES.get(name, "eval.cu: " + str(name))
     return "other (" + f + ")"
 
 
