@@ -304,6 +304,13 @@ const char* kitc_last_error(void);
  * (monotone counter; bench.py reports the difference over the timed region). */
 uint64_t kitc_launch_count(void);
 
+/* Build flags of the loaded library: bit 0 (KITC_BUILD_CHECKS) = device-side invariant
+ * checks compiled in (the verification build libkitc_checks.so: index bounds of the
+ * traversal, TMA stages, scatter and weights work items; a violation traps and the next
+ * synchronising call returns KITC_ECUDA).  0 for the product build. */
+#define KITC_BUILD_CHECKS 1
+uint32_t kitc_build_flags(void);
+
 #ifdef __cplusplus
 }
 #endif

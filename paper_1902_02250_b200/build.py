@@ -8,6 +8,9 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libkitc.so")
+# verification build: the same sources with the device-side invariant checks compiled in
+# (KITC_CHECKS, csrc/kitc_internal.cuh); loaded only by tests/test_gpu_checks.py via KITC_LIB
+CHECKS_LIB = os.path.join(HERE, "libkitc_checks.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared"]
 
@@ -29,23 +32,25 @@ def build_id() -> str:
     return h.hexdigest()[:16]
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not (force or stale()):
-        return LIB
+def build(force: bool = False, verbose: bool = False, checks: bool = False) -> str:
+    """libkitc.so (checks=False) or the verification build libkitc_checks.so (checks=True)."""
+    lib = CHECKS_LIB if checks else LIB
+    if not (force or stale(lib)):
+        return lib
     nvcc = os.environ.get("NVCC", "nvcc")
     if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
         nvcc = "/usr/local/cuda/bin/nvcc"
     cus = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
-    objdir = os.path.join(ROOT, "build", "kitc_obj")
+    objdir = os.path.join(ROOT, "build", "kitc_checks_obj" if checks else "kitc_obj")
     os.makedirs(objdir, exist_ok=True)
-    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"] + (["-DKITC_CHECKS"] if checks else [])
     jobs = []
     for cu in cus:  # one nvcc per translation unit, in parallel (eval.cu dominates)
         obj = os.path.join(objdir, os.path.basename(cu) + ".o")
@@ -58,13 +63,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if proc.wait() != 0:
             raise subprocess.CalledProcessError(proc.returncode, "nvcc -c " + obj)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     if verbose:
         print(" ".join(link))
     subprocess.check_call(link)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 PROBE_SRC = os.path.join(ROOT, "tools", "fp64_peak.cu")

@@ -82,3 +82,11 @@ void HostBuf::release() {
 extern "C" const char* kitc_last_error(void) { return kitc::g_last_error.c_str(); }
 
 extern "C" uint64_t kitc_launch_count(void) { return kitc::g_launches.load(); }
+
+extern "C" uint32_t kitc_build_flags(void) {
+#ifdef KITC_CHECKS
+    return KITC_BUILD_CHECKS;
+#else
+    return 0;
+#endif
+}

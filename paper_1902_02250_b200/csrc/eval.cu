@@ -123,6 +123,8 @@ struct EvalArgs {
     long long bb, be;
     int part, nparts;  // interleaved multi-GPU split (nparts > 1): chunks of kPartChunk batches
     int N;
+    int ncl;   // clusters in the tree (index bound; KITC_CHECKS)
+    long long nout;  // output rows (index bound; KITC_CHECKS)
     int P;  // n + 1 (runtime copy)
     int stack_cap;
     int warp_smem;  // bytes of shared memory per warp (WarpSmem)
@@ -141,6 +143,7 @@ struct WarpSmem {
     unsigned long long* bar;   // 2 mbarriers
     int* nround;
     int2* stk;
+    int stage_bytes;  // bytes available for the two stage buffers (KITC_CHECKS)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -194,6 +197,7 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
     const int base = *ws.nround;
     auto issue = [&](int st, int k) {  // stage st of this cluster -> buffer k & 1
         const int nb = min(kSB, R - st * kSB);
+        KITC_DCHECK(nb >= 1 && (st * kSB + nb) * blk <= R * blk && 2 * kSB * blk * 8 <= ws.stage_bytes);
         tma_round(ws.buf + (k & 1) * kSB * blk, F + (size_t)st * kSB * blk, (unsigned)(nb * blk * 8),
                   ws.bar + (k & 1));
     };
@@ -451,6 +455,7 @@ __device__ __forceinline__ void far_field_team(double x, double y, double z, con
     const int base = *ws.nround;
     auto issue = [&](int st, int k) {
         const int nb = min(kSB, R - st * kSB);
+        KITC_DCHECK(nb >= 1 && (st * kSB + nb) * blk <= R * blk && 2 * kSB * blk * 8 <= ws.stage_bytes);
         tma_round(ws.buf + (k & 1) * kSB * blk, F + (size_t)st * kSB * blk, (unsigned)(nb * blk * 8),
                   ws.bar + (k & 1));
     };
@@ -723,6 +728,7 @@ __device__ __forceinline__ void near_leaf(double x, double y, double z, int t, i
     constexpr int NA = K::NA;
     const int grp = lane % kGroup, g = lane / kGroup;
     const int nt = __popc(rm) / kGroup;
+    KITC_DCHECK(b >= 0 && b <= e && e <= a.N && (rm & 0x01010101u) * 0xffu == rm);
     const bool mine = (rm >> lane) & 1u;
     constexpr bool kTB = ((KITC_NEAR_TB >> KER) & 1) ||
                          (KITC_NEAR_TB_AT4 && KER == 0 && eval_min_blocks<PT, KER>() == 4);
@@ -814,6 +820,8 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
         ws.nround = reinterpret_cast<int*>(ws.bar + 2);
         ws.dzs = reinterpret_cast<double*>(ws.bar + 3);
         ws.stk = reinterpret_cast<int2*>(ws.dzs + (KITC_DZ_SMEM ? kBatch * P : 0));
+        ws.stage_bytes = (int)(reinterpret_cast<unsigned char*>(ws.bar) - base);
+        KITC_DCHECK(reinterpret_cast<unsigned char*>(ws.stk + a.stack_cap) <= base + a.warp_smem);
         if (lane == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(ws.bar)));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(ws.bar + 1)));
@@ -837,8 +845,10 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
         p0 = (int)(b * kBatch);
         tc = (int)min((long long)kBatch, a.nt - p0);
     }
+    KITC_DCHECK(p0 >= 0 && tc >= 1 && tc <= kBatch && (long long)p0 + tc <= a.nt);
     const bool valid = ti < tc;
     const int t = a.tord ? a.tord[p0 + (valid ? ti : 0)] : p0 + (valid ? ti : 0);
+    KITC_DCHECK(t >= 0 && t < a.nt);
     const double x = a.tx[t], y = a.ty[t], z = a.tz[t];
     const int P = PT > 0 ? PT : a.P;
     const int P3 = P * P * P;
@@ -857,6 +867,7 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
         __syncwarp();
         const int c = ent.x;
         const unsigned mask = (unsigned)ent.y;
+        KITC_DCHECK(c >= 0 && c < a.ncl && (mask & ~live) == 0u);
         const bool in = (mask >> lane) & 1u;
         const double4 cr = a.cr[c];
         bool ok = false;
@@ -868,6 +879,9 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
         const unsigned am = __ballot_sync(0xffffffffu, ok);
         const unsigned rm = mask & ~am;
         const int4 tp = a.topo[c];
+        // a cluster's particles lie in [0, N); children (BFS numbering) follow their parent
+        KITC_DCHECK(tp.x >= 0 && tp.x <= tp.y && tp.y <= a.N && tp.w >= 0 && tp.w <= 8 &&
+                    (tp.w == 0 || (tp.z > c && tp.z + tp.w <= a.ncl)));
 #ifdef KITC_EVAL_HIST
         // tuning only: histogram of accepting targets per (warp, far cluster) and of
         // near-field participants per (warp, leaf) -> g_hist[0..4], g_hist[5..9]
@@ -933,6 +947,7 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
         for (int o = 1; o < kGroup; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
     if (!valid || grp != 0) return;
     const int o = a.perm[t];
+    KITC_DCHECK(o >= 0 && o < a.nout);
 #pragma unroll
     for (int c = 0; c < NP; ++c) a.out[(size_t)o * NP + c] = K::out(acc, c);
     if (STATS)
@@ -1033,6 +1048,8 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     a.part = part;
     a.nparts = nparts;
     a.N = (int)t->N;
+    a.ncl = (int)t->nclusters;
+    a.nout = ts ? ts->n : t->N;
     a.P = n + 1;
     a.stack_cap = 8 * (t->depth + 1);
     a.self_omit = self == KITC_SELF_OMIT;

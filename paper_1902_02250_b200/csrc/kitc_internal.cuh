@@ -29,6 +29,25 @@ inline long long fhat_cluster_len(int P, int M) { return (long long)fhat_rounds(
 extern std::atomic<unsigned long long> g_launches;  // kernels launched by the library
 inline void note_launch(unsigned long long n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// ---- device-side invariant checks (verification builds: -DKITC_CHECKS) ------
+// A violated index bound prints its location and traps; the next synchronising call
+// reports KITC_ECUDA.  tests/test_gpu_checks.py runs the parity cases on such a build
+// (compute-sanitizer is not available on the GPU pool).  Compiled out by default.
+#ifdef KITC_CHECKS
+#include <cstdio>
+#define KITC_DCHECK(cond)                                                            \
+    do {                                                                             \
+        if (!(cond)) {                                                               \
+            printf("KITC_CHECKS %s:%d: %s\n", __FILE__, __LINE__, #cond);            \
+            __trap();                                                                \
+        }                                                                            \
+    } while (0)
+#else
+#define KITC_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 // ---- error plumbing ---------------------------------------------------------
 kitc_status set_error(kitc_status st, const std::string& msg);
 kitc_status check_cuda(cudaError_t e, const char* what);

@@ -571,6 +571,7 @@ __global__ void __launch_bounds__(kBT, 1) k_build(const BuildArgs a) {
                             const int code = valid ? child_code(px[u], py[u], pz[u], sp) : 8;
                             const unsigned peers = __match_any_sync(0xffffffffu, code);
                             const int pos = __shfl_sync(0xffffffffu, base, code & 7) + __popc(peers & lt);
+                            KITC_DCHECK(!valid || (pos >= tp.x && pos < tp.y));  // children partition the parent
                             if (valid) {
                                 nx[pos] = px[u];
                                 ny[pos] = py[u];
@@ -625,6 +626,7 @@ __global__ void __launch_bounds__(kBT, 1) k_build(const BuildArgs a) {
                             if (valid) {
                                 int pos = sm.sc.base[code] + rank;
                                 for (int k = 0; k < w; ++k) pos += sm.sc.wcnt[k][code];
+                                KITC_DCHECK(pos >= tp.x && pos < tp.y);  // children partition the parent
                                 nx[pos] = px[u];
                                 ny[pos] = py[u];
                                 nz[pos] = pz[u];

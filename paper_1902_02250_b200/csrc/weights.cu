@@ -141,6 +141,7 @@ __global__ void __launch_bounds__((P * P + 31) / 32 * 32, P <= 11 ? KITC_W_MINB 
     __shared__ double Lx[kTile][P], Ly[kTile][P], Lz[kTile][P], sw[kTile][M];
     if ((int)blockIdx.x >= *nitems) return;  // grid sized by an upper bound (no host sync)
     const WItem it = items[blockIdx.x];
+    KITC_DCHECK(it.b >= 0 && it.b <= it.e && it.e <= N && it.c >= 0);
     const int tid = threadIdx.x;
     for (int i = tid; i < 3 * P; i += NT) sg[i] = grid[(size_t)it.c * 3 * P + i];
     const int k2 = tid / P, k3 = tid % P;

@@ -33,7 +33,7 @@ EXPORTS = ("kitc_kernel_dims", "kitc_fhat_cluster_len", "kitc_tree_create", "kit
            "kitc_tree_workspace_bytes", "kitc_build_tree", "kitc_tree_info",
            "kitc_tree_export", "kitc_modified_weights", "kitc_modified_weights_ex", "kitc_modified_weights_peers", "kitc_eval", "kitc_eval_ex", "kitc_eval_part", "kitc_eval_targets", "kitc_eval_targets_ex", "kitc_batch_targets",
            "kitc_direct", "kitc_direct_sample", "kitc_rel_error", "kitc_tree_free", "kitc_last_error",
-           "kitc_launch_count")
+           "kitc_launch_count", "kitc_build_flags")
 
 
 class KitcError(RuntimeError):
@@ -96,6 +96,7 @@ def _load():
         "kitc_tree_free": [vp],
         "kitc_last_error": [],
         "kitc_launch_count": [],
+        "kitc_build_flags": [],
     }
     global SIGNATURES
     SIGNATURES = sig
@@ -106,6 +107,7 @@ def _load():
     L.kitc_tree_free.restype = None
     L.kitc_last_error.restype = C.c_char_p
     L.kitc_launch_count.restype = C.c_uint64
+    L.kitc_build_flags.restype = C.c_uint32
     return L
 
 
@@ -249,6 +251,11 @@ def kitc_rel_error(ref_ptr, approx_ptr, count, scratch_ptr, stream_ptr):
 
 def kitc_launch_count():
     return int(_lib.kitc_launch_count())
+
+
+def kitc_build_flags():
+    """Bit 0 (KITC_BUILD_CHECKS): the loaded library is the verification build."""
+    return int(_lib.kitc_build_flags())
 
 
 def kitc_tree_free(t):

@@ -170,3 +170,17 @@ def test_tree_workspace_bytes():
         with pytest.raises(kitc.KitcError) as e:
             kitc.kitc_tree_workspace_bytes(*bad)
         assert e.value.status == kitc.KITC_EINVAL
+
+
+def test_product_library_has_the_checks_compiled_out():
+    # libkitc.so is the product build (KITC_BUILD_CHECKS clear); libkitc_checks.so, the
+    # verification build tests/test_gpu_checks.py loads, sets it.  No CUDA call is made.
+    import ctypes
+    from paper_1902_02250_b200 import build as B, kitc
+    if os.environ.get("KITC_LIB"):
+        pytest.skip("a tuning / verification library is loaded")
+    assert kitc.kitc_build_flags() == 0
+    if os.path.exists(B.CHECKS_LIB):
+        lib = ctypes.CDLL(B.CHECKS_LIB)
+        lib.kitc_build_flags.restype = ctypes.c_uint32
+        assert lib.kitc_build_flags() == 1

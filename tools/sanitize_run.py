@@ -29,4 +29,4 @@ for (N, N0, n, kern, geom) in [(3001, 60, 8, 0, "uniform"), (2000, 40, 4, 1, "sp
     kitc.direct_sample(dev(X), dev(W), kern, 0.02, torch.arange(0, N, 3, device="cuda"))
     print(N, geom, "E", kitc.rel_error(d, u))
 torch.cuda.synchronize()
-print("sanitize run ok")
+print("sanitize run ok, build flags", kitc.kitc_build_flags(), "library", kitc.LIB_PATH)
