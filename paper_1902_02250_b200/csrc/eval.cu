@@ -413,6 +413,88 @@ __device__ __forceinline__ void far_field(double x, double y, double z, const do
 #undef KITC_DZ
 }
 
+#ifndef KITC_FAR_SMALL
+#define KITC_FAR_SMALL 1  // Stokeslet at P <= 8: the whole cluster in one stage (far_small)
+#endif
+__host__ __device__ constexpr bool far_small_on(int P, int KER) {
+    return KITC_FAR_SMALL && KER == 0 && P >= 2 && P <= 8;
+}
+// f-hat blocks of stage buffer per warp: the whole cluster (far_small) or two kSB-block stages
+__host__ __device__ constexpr int stage_blocks(int P, int KER) {
+    return far_small_on(P, KER) && (P * P + kRows - 1) / kRows > 2 * kSB ? (P * P + kRows - 1) / kRows : 2 * kSB;
+}
+
+// Far field of one accepted cluster at low degree (Stokeslet, P <= 8): the cluster's f-hat
+// (R blocks of 8 rows) comes in ONE bulk copy with one wait, and every lane of a target group
+// sums the rows grp, grp + 8, grp + 16, .. of the full blocks in groups of RG independent row
+// chains (RG = all of them when there are <= 3, else 2), the P^2 mod 8 leftover rows pair by
+// pair.  Against far_field's two-block stages this drops the per-stage handshake and the
+// one-row-per-lane stage: far-field loop alone (tools/far_small_probe.cu, all 4 targets
+// accepting) P = 4 46.5 -> 50.0%, P = 5 49.9 -> 56.2%, P = 6 52.7 -> 57.0%, P = 7 60.3 -> 63.5%,
+// P = 8 (vs target pairs) 67.8 -> 70.0% of the FP64 peak.  The stage is one round of the
+// warp's round counter, so it interleaves with far_field_team's two-buffer rounds.
+template <int PT, int KER>
+__device__ __forceinline__ void far_small(double x, double y, double z, const double* __restrict__ g,
+                                          const double* __restrict__ F, double* acc, const KParams& kp, int grp,
+                                          int lane, unsigned am, const WarpSmem& ws) {
+    using K = EvalKern<KER>;
+    constexpr int P = PT, M = K::M, P2 = P * P, R = (P2 + kRows - 1) / kRows, RF = P2 / kRows;
+    constexpr int blk = P * M * kRows, RG = RF <= 3 ? (RF > 0 ? RF : 1) : 2;
+    static_assert(RF <= 3 || RF % 2 == 0, "far_small: row groups of 2");
+    const int k = *ws.nround;
+    if (lane == __ffs(am) - 1) {
+        KITC_DCHECK(R * blk * 8 <= ws.stage_bytes);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // buffer last read by the generic proxy
+        tma_round(ws.buf, F, (unsigned)(R * blk * 8), ws.bar + (k & 1));
+    }
+    double dzr[P];
+#pragma unroll
+    for (int k3 = 0; k3 < P; ++k3) dzr[k3] = z - __ldg(g + 2 * P + k3);
+    mbar_wait(ws.bar + (k & 1), (unsigned)(k >> 1) & 1u);
+    const double* B = ws.buf;
+#pragma unroll 1
+    for (int r0 = 0; r0 < RF; r0 += RG) {
+        double dx[RG], dy[RG], pp[RG];
+        typename K::Row rw[RG];
+#pragma unroll
+        for (int i = 0; i < RG; ++i) {
+            const int row = (r0 + i) * kRows + grp, k1 = row / P, k2 = row - k1 * P;
+            dx[i] = x - __ldg(g + k1);
+            dy[i] = y - __ldg(g + P + k2);
+            pp[i] = fma(dy[i], dy[i], dx[i] * dx[i]) + kp.e2;
+        }
+#pragma unroll
+        for (int k3 = 0; k3 < P; ++k3) {
+            const double zk = dzr[k3];
+#pragma unroll
+            for (int i = 0; i < RG; ++i) {
+                double f[M];
+#pragma unroll
+                for (int m = 0; m < M; ++m) f[m] = B[((r0 + i) * P + k3) * M * kRows + m * kRows + grp];
+                K::pair_row(dx[i], dy[i], zk, fma(zk, zk, pp[i]), f, acc, rw[i], kp);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < RG; ++i) K::row_end(dx[i], dy[i], rw[i], acc);
+    }
+    if constexpr (P2 > RF * kRows) {  // the partial block's rows, pair by pair over the group's lanes
+        const double* Bb = B + RF * blk;
+        constexpr int pairs = (P2 - RF * kRows) * P;
+        for (int q = grp; q < pairs; q += kRows) {
+            const int jj = q / P, k3 = q - jj * P, row = RF * kRows + jj;
+            const int k1 = row / P, k2 = row - k1 * P;
+            const double ddx = x - __ldg(g + k1), ddy = y - __ldg(g + P + k2), dzk = z - __ldg(g + 2 * P + k3);
+            double f[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) f[m] = Bb[(k3 * M + m) * kRows + jj];
+            K::pair(ddx, ddy, dzk, fma(ddy, ddy, ddx * ddx) + fma(dzk, dzk, kp.e2), f, acc, kp);
+        }
+    }
+    __syncwarp(am);  // every accepted lane is done with the buffer
+    if (lane == __ffs(am) - 1) *ws.nround = k + 1;
+    __syncwarp(am);
+}
+
 // Far field of one cluster accepted by only 1 or 2 of the batch's targets, by the
 // WHOLE warp ("teams", as near_leaf): the idle target groups join the accepting
 // ones.  Two targets: teams of 16 lanes, one row of the 16-row stage per lane.
@@ -816,7 +898,8 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
         const int blk = P * M * kRows;
         unsigned char* base = smem_raw + (size_t)wl * a.warp_smem;
         ws.buf = reinterpret_cast<double*>(base);
-        ws.bar = reinterpret_cast<unsigned long long*>(base + 2 * kSB * blk * sizeof(double));
+        ws.bar = reinterpret_cast<unsigned long long*>(base + (PT > 0 ? stage_blocks(PT, KER) : 2 * kSB) * blk *
+                                                                     sizeof(double));
         ws.nround = reinterpret_cast<int*>(ws.bar + 2);
         ws.dzs = reinterpret_cast<double*>(ws.bar + 3);
         ws.stk = reinterpret_cast<int2*>(ws.dzs + (KITC_DZ_SMEM ? kBatch * P : 0));
@@ -910,8 +993,12 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
                 st[4] += (unsigned long long)(tp.y - tp.x);
             }
         } else if (am && ok) {
-            far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * LEN, acc, a.kp, P, grp,
-                               lane, am, ws);
+            if constexpr (PT > 0 && far_small_on(PT, KER))
+                far_small<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * LEN, acc, a.kp, grp,
+                                   lane, am, ws);
+            else
+                far_field<PT, KER>(x, y, z, a.grid + (size_t)c * 3 * P, a.fhat + (size_t)c * LEN, acc, a.kp, P,
+                                   grp, lane, am, ws);
             if (STATS) {
                 st[0] += 1;
                 st[1] += (unsigned long long)P3;
@@ -1060,7 +1147,8 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     KITC_TRY(kitc_kernel_dims(kernel, &m, nullptr));
     if (reinterpret_cast<uintptr_t>(fhat) % 16) return set_error(KITC_EINVAL, "kitc_eval: fhat must be 16-byte aligned");
     // per warp: 2 stage buffers + 2 mbarriers + round counter (8 B) + stack, 128-B multiple
-    a.warp_smem = (int)(((size_t)2 * kSB * (n + 1) * m * kRows * sizeof(double) + 24 + (size_t)a.stack_cap * sizeof(int2) +
+    a.warp_smem = (int)(((size_t)stage_blocks(n + 1, kernel) * (n + 1) * m * kRows * sizeof(double) + 24 +
+                         (size_t)a.stack_cap * sizeof(int2) +
                          (KITC_DZ_SMEM ? (size_t)kBatch * (n + 1) * sizeof(double) : 0) +
                          127) / 128 * 128);
     const size_t smem = (size_t)kWarps * a.warp_smem;
