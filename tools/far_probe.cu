@@ -731,7 +731,8 @@ void run(int sms, int clk_khz) {
     cudaMemcpy(s, hs.data(), nseq * 4, cudaMemcpyHostToDevice);
     const int warp_smem = (int)(((size_t)2 * kSB * P * M * kRows * 8 + 24 + 64 * 8 + (size_t)kBatch * P * 8 + 127) /
                                 128 * 128);
-    const size_t smem = (size_t)kWarps * warp_smem;
+    // FAR_PROBE_EXTRA_SMEM (bytes per CTA): enlarge the shared-memory carve-out (less L1) without using it
+    const size_t smem = (size_t)kWarps * warp_smem + (getenv("FAR_PROBE_EXTRA_SMEM") ? atoi(getenv("FAR_PROBE_EXTRA_SMEM")) : 0);
     cudaFuncSetAttribute(k_far_probe<PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_far_tb<PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_far_var<PT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
