@@ -197,8 +197,11 @@ __device__ __forceinline__ void far_stages(double x, double y, double z, const d
     __syncwarp();
 }
 
+#ifndef FSP_MINB
+#define FSP_MINB 4
+#endif
 template <int PT, int KER, int V>
-__global__ void __launch_bounds__(kWarps * 32, 4)
+__global__ void __launch_bounds__(kWarps * 32, FSP_MINB)
     k_probe(const double* grid, const double* fhat, const int* seq, int nseq, int ncalls, double* out, KParams kp,
             int warp_smem) {
     constexpr int M = EvalKern<KER>::M, P = PT, NA = EvalKern<KER>::NA;
@@ -279,18 +282,25 @@ void run(int sms, int clk_khz) {
     cudaFuncSetAttribute(k_probe<PT, KER, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_probe<PT, KER, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_probe<PT, KER, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_probe<PT, KER, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int ctas = sms * 4 * 8, ncalls = 192;
     const KParams kp = make_kparams(0.01);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
+#ifdef FSP_BIG
+    const int VS[4] = {0, 2, 5, 0};
+#else
     const int VS[4] = {0, 6, 7, 8};
+#endif
     for (int rep = 0; rep < 8; ++rep) {
         const int V = VS[rep % 4];
         cudaEventRecord(e0);
         if (V == 0) k_probe<PT, KER, 0><<<ctas, kWarps * 32, smem>>>(g, f, s, nseq, ncalls, o, kp, warp_smem);
         else if (V == 6) k_probe<PT, KER, 6><<<ctas, kWarps * 32, smem>>>(g, f, s, nseq, ncalls, o, kp, warp_smem);
         else if (V == 7) k_probe<PT, KER, 7><<<ctas, kWarps * 32, smem>>>(g, f, s, nseq, ncalls, o, kp, warp_smem);
+        else if (V == 2) k_probe<PT, KER, 2><<<ctas, kWarps * 32, smem>>>(g, f, s, nseq, ncalls, o, kp, warp_smem);
+        else if (V == 5) k_probe<PT, KER, 5><<<ctas, kWarps * 32, smem>>>(g, f, s, nseq, ncalls, o, kp, warp_smem);
         else k_probe<PT, KER, 8><<<ctas, kWarps * 32, smem>>>(g, f, s, nseq, ncalls, o, kp, warp_smem);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
@@ -301,7 +311,7 @@ void run(int sms, int clk_khz) {
         const double fl = KER == 0 ? 32 : 59;
         if (rep >= 4)
             printf("K %d P %2d %-18s %.3f ms, %.3f pairs/clk/SM, %.1f%% of %.2f TFLOP/s (err %s)\n", KER, P,
-                   V == 0 ? "far_field (prod)" : V == 6 ? "stages 6 blk x1 buf" : V == 7 ? "stages 3 blk x2 buf" : "stages 4 blk x1 buf", ms,
+                   V == 0 ? "far_field (prod)" : V == 6 ? "stages 6 blk x1 buf" : V == 7 ? "stages 3 blk x2 buf" : V == 2 ? "whole cluster RG2" : V == 5 ? "whole cluster RG5" : "stages 4 blk x1 buf", ms,
                    rate / (sms * clk_khz * 1e3), 100.0 * rate * fl / (sms * 128.0 * clk_khz * 1e3),
                    sms * 128.0 * clk_khz * 1e-9,
                    cudaGetErrorString(cudaGetLastError()));
