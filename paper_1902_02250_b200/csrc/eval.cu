@@ -12,8 +12,9 @@
 //         modified weights fhat_k (Eq. pc_approximation_3D): fhat
 //         staged into shared memory by cp.async.bulk (TMA) two stages ahead,
 //         tensor-product reuse of dx, dy, dz, two rows per lane (far_field) or,
-//         for the Stokeslet at P = 8, 10 with all 4 targets accepting, one row
-//         for two targets per lane; a cluster accepted by only 1 or 2 targets is
+//         for the Stokeslet at P = 10 with all 4 targets accepting, one row for
+//         two targets per lane; for the Stokeslet at P <= 8 the whole cluster in
+//         one stage (far_small); a cluster accepted by only 1 or 2 targets is
 //         done by the whole warp (far_field_team)
 //   near  rejecting lanes at a leaf sum over its particles directly
 //         (Eq. pc_interaction_3D), j == i skipped by index (reading A8); idle
@@ -72,8 +73,8 @@ namespace {
 #endif
 #ifndef KITC_FAR_TB
 // far field with all 4 targets accepting: one row for TWO targets per lane, Stokeslet at
-// P = 8, 10 (measured on the C3 input: n = 7 -8%, n = 9 -6%; slower at P = 9 (spills at
-// 5 CTAs/SM, 4 CTAs/SM loses more), P = 11, P <= 7 and for the rotlet)
+// P = 10 (measured on the C3 input: n = 9 -6%; slower at P = 9 (spills at 5 CTAs/SM, 4 CTAs/SM
+// loses more), P = 11, P <= 7 and for the rotlet; at P = 8 (n = 7 -8%) superseded by far_small)
 #define KITC_FAR_TB 1
 #endif
 #ifndef KITC_FAR_TB_P9

@@ -152,6 +152,25 @@ def test_treecode_parity(K, N, N0, n, theta, kern, eps, geom):
     assert np.array_equal(rst.astype(np.int64), gst)
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7])
+def test_far_small_every_degree(K, n):
+    # eval.cu far_small (Stokeslet, P = n + 1 <= 8: the whole cluster in one stage, row groups of
+    # 1 / 2 / 3 chains, leftover rows pair by pair) with the accepting masks that occur naturally
+    # (all 4 targets, 3 of 4 through far_small; 1 or 2 through the team path): many small clusters
+    # so partial masks are frequent; sources as targets and separate targets
+    X, W = KI.particles(6000, "sphere", seed=20 + n)
+    T = O.Tree(X, 40)
+    ref, rst = T.treecode(0, 0.02, n, 0.8, W, stats=True)
+    got, gst, G = run_gpu(K, X, W, 0, n, 0.8, 40, 0.02)
+    assert O.rel_error(ref, got) <= TREE_GATE, n
+    assert np.array_equal(rst.astype(np.int64), gst)
+    Xt = np.random.default_rng(n).uniform(-1.2, 1.2, (700, 3))
+    reft = T.treecode_targets(0, 0.02, n, 0.8, W, Xt)
+    fh = G.modified_weights(0, n, dev(W))
+    gott = host(G.eval_targets(0, n, 0.8, 0.02, fh, dev(Xt)))
+    assert O.rel_error(reft, gott) <= TREE_GATE, n
+
+
 def test_treecode_self_include(K):
     X, W = KI.particles(4000, seed=2)
     T = O.Tree(X, 150)
