@@ -107,6 +107,7 @@ struct EvalArgs {
     const double* tx;  // targets by position t (= x, y, z when targets = sources)
     const double* ty;
     const double* tz;
+    int tpack;  // 1: targets = sources, coordinates read from the packed records (src)
     const int* perm;  // output row of target position t
     const int* tord;  // batch slot -> target position (nullptr: identity)
     const double* w;  // sorted weights, M planes of N
@@ -933,7 +934,18 @@ __global__ void __launch_bounds__(kWarps * 32, eval_min_blocks<PT, KER>()) k_eva
     const bool valid = ti < tc;
     const int t = a.tord ? a.tord[p0 + (valid ? ti : 0)] : p0 + (valid ? ti : 0);
     KITC_DCHECK(t >= 0 && t < a.nt);
-    const double x = a.tx[t], y = a.ty[t], z = a.tz[t];
+    double x, y, z;
+    if (a.tpack) {  // targets = sources: the coordinates from the packed record (no separate read of x, y, z)
+        const double* r = a.src + (size_t)t * a.sld;
+        const double2 xy = __ldg(reinterpret_cast<const double2*>(r));
+        x = xy.x;
+        y = xy.y;
+        z = __ldg(r + 2);
+    } else {
+        x = a.tx[t];
+        y = a.ty[t];
+        z = a.tz[t];
+    }
     const int P = PT > 0 ? PT : a.P;
     const int P3 = P * P * P;
     const long long LEN = (long long)((P * P + kRows - 1) / kRows) * P * M * kRows;  // fhat doubles per cluster
@@ -1109,6 +1121,7 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
     a.tx = a.x;
     a.ty = a.y;
     a.tz = a.z;
+    a.tpack = 1;
     a.w = t->w.as<double>();
     a.src = t->src.as<double>();
     a.sld = t->src_ld;
@@ -1123,6 +1136,7 @@ kitc_status eval(const kitc_tree* t, int kernel, int n, double theta, double eps
         a.tx = ts->x;
         a.ty = ts->y;
         a.tz = ts->z;
+        a.tpack = 0;
         a.perm = ts->row;
         a.tord = nullptr;
         a.bstart = a.bcount = nullptr;
