@@ -137,8 +137,15 @@ __global__ void __launch_bounds__((P * P + 31) / 32 * 32, P <= 11 ? KITC_W_MINB 
     const Peers fhat, double* __restrict__ part, const int* __restrict__ nitems) {
     constexpr int P2 = P * P, NT = (P2 + 31) / 32 * 32, R = (P2 + kRows - 1) / kRows;
     constexpr int LEN = R * P * M * kRows;
+    // rows padded to an even length: the x vector and the weights are read as 16-byte pairs
+    constexpr int PP = (P + 1) & ~1, MP = (M + 1) & ~1;
+    constexpr int QC = (3 * kTile + NT - 1) / NT, QW = (M * kTile + NT - 1) / NT;  // phase-1 items per thread
     __shared__ double sg[3 * P];
-    __shared__ double Lx[kTile][P], Ly[kTile][P], Lz[kTile][P], sw[kTile][M];
+    // two tile buffers: phase 1 of tile t + 1 fills one while no thread can still read it
+    // (they all passed tile t's barrier after finishing phase 2 of tile t - 1) -> one barrier per tile
+    __shared__ __align__(16) double Lx[2][kTile][PP];
+    __shared__ double Ly[2][kTile][P], Lz[2][kTile][P];
+    __shared__ __align__(16) double sw[2][kTile][MP];
     if ((int)blockIdx.x >= *nitems) return;  // grid sized by an upper bound (no host sync)
     const WItem it = items[blockIdx.x];
     KITC_DCHECK(it.b >= 0 && it.b <= it.e && it.e <= N && it.c >= 0);
@@ -151,33 +158,61 @@ __global__ void __launch_bounds__((P * P + 31) / 32 * 32, P <= 11 ? KITC_W_MINB 
     for (int m = 0; m < M; ++m)
 #pragma unroll
         for (int k = 0; k < P; ++k) acc[m][k] = 0.0;
-    __syncthreads();
-    for (int tile = it.b; tile < it.e; tile += kTile) {
+    // the next tile's coordinates and weights, loaded into registers one tile ahead (their
+    // global latency overlaps phase 2 of the current tile)
+    double pc[QC], pw[QW];
+    auto prefetch = [&](int tile) {
         const int cnt = min(kTile, it.e - tile);
-        // phase 1: the 3 cnt per-axis vectors spread over all threads
-        for (int q = tid; q < 3 * cnt; q += NT) {
-            const int l = q / cnt, j = q - l * cnt, i = tile + j;
-            const double* coord = l == 0 ? x : l == 1 ? y : z;
-            double(*L)[P] = l == 0 ? Lx : l == 1 ? Ly : Lz;
-            bary<P>(coord[i], sg + l * P, L[j]);
+#pragma unroll
+        for (int i = 0; i < QC; ++i) {
+            const int q = tid + i * NT, l = q / cnt, j = q - l * cnt;
+            if (q < 3 * cnt) pc[i] = (l == 0 ? x : l == 1 ? y : z)[tile + j];
         }
-        for (int q = tid; q < M * cnt; q += NT) {
-            const int m = q / cnt, j = q - m * cnt;
-            sw[j][m] = ws[(size_t)m * N + tile + j];
+#pragma unroll
+        for (int i = 0; i < QW; ++i) {
+            const int q = tid + i * NT, m = q / cnt, j = q - m * cnt;
+            if (q < M * cnt) pw[i] = ws[(size_t)m * N + tile + j];
         }
+    };
+    if (it.b < it.e) prefetch(it.b);
+    __syncthreads();
+    int buf = 0;
+    for (int tile = it.b; tile < it.e; tile += kTile, buf ^= 1) {
+        const int cnt = min(kTile, it.e - tile);
+        // phase 1: the 3 cnt per-axis vectors and the cnt weights, spread over all threads
+#pragma unroll
+        for (int i = 0; i < QC; ++i) {
+            const int q = tid + i * NT, l = q / cnt, j = q - l * cnt;
+            if (q < 3 * cnt) bary<P>(pc[i], sg + l * P, l == 0 ? Lx[buf][j] : l == 1 ? Ly[buf][j] : Lz[buf][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < QW; ++i) {
+            const int q = tid + i * NT, m = q / cnt, j = q - m * cnt;
+            if (q < M * cnt) sw[buf][j][m] = pw[i];
+        }
+        if (tile + kTile < it.e) prefetch(tile + kTile);
         __syncthreads();
         if (owner) {
             for (int j = 0; j < cnt; ++j) {
-                const double q = Ly[j][k2] * Lz[j][k3];
+                const double q = Ly[buf][j][k2] * Lz[buf][j][k3];
+                double g[MP];
 #pragma unroll
-                for (int m = 0; m < M; ++m) {
-                    const double g = q * sw[j][m];
+                for (int m = 0; m < MP; m += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(&sw[buf][j][m]);
+                    g[m] = q * v.x;
+                    g[m + 1] = q * v.y;
+                }
 #pragma unroll
-                    for (int k1 = 0; k1 < P; ++k1) acc[m][k1] = fma(Lx[j][k1], g, acc[m][k1]);
+                for (int k1 = 0; k1 < PP; k1 += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(&Lx[buf][j][k1]);
+#pragma unroll
+                    for (int m = 0; m < M; ++m) {
+                        acc[m][k1] = fma(v.x, g[m], acc[m][k1]);
+                        if (k1 + 1 < P) acc[m][k1 + 1] = fma(v.y, g[m], acc[m][k1 + 1]);
+                    }
                 }
             }
         }
-        __syncthreads();
     }
     const int nd = it.slot < 0 ? fhat.n : 1;
     for (int r = 0; r < nd; ++r) {
