@@ -1,5 +1,5 @@
 """Eval throughput over (n, theta) on the C3 input (N = 1e6 uniform, N0 = 2000, Stokeslet and rotlet):
-eval ms, pairs/target, % of the derived FP64 peak.  [PM_N=4,6 PM_THETA=0.7] python tools/perf_matrix.py"""
+eval ms, pairs/target, % of the derived FP64 peak.  [PM_N=4,6 PM_THETA=0.7 PM_KERN=0] python tools/perf_matrix.py"""
 import json
 import os
 import sys
@@ -18,7 +18,7 @@ G = kitc.Tree(Xd, 2000)
 rows = []
 NS = [int(v) for v in os.environ.get("PM_N", "4,6,8,10").split(",")]
 THETAS = [float(v) for v in os.environ.get("PM_THETA", "0.5,0.7").split(",")]
-for kern in (0, 1):
+for kern in [int(v) for v in os.environ.get("PM_KERN", "0,1").split(",")]:
     for n in NS:
         fh = G.modified_weights(kern, n, Wd)
         for theta in THETAS:
